@@ -1,0 +1,197 @@
+/*
+ * dg_b200.h -- C ABI of the B200-native densegraph hot path.
+ *
+ * The reference (densegraph, arXiv 2311.04333 artifact) exposes its hot path
+ * as a C++ library API (proj/include/densegraph/*.hpp).  This header is the
+ * drop-in boundary underneath that API: plain pointers and sizes, no C++ or
+ * torch types, status codes instead of exceptions.  include/densegraph/*.hpp
+ * re-creates the reference's C++ API on top of it, so reference callers
+ * (its CLI and tests) compile unchanged; INTEGRATION.md shows the binding.
+ *
+ * Every call is externally synchronous (returns finished results), like the
+ * reference.  The library owns all device memory behind dg_graph handles;
+ * callers own host buffers, sized from dg_graph_info.  Unless a parameter
+ * says "device", pointers are host pointers.  Handles are immutable.
+ *
+ * There is no CPU fallback: every computing entry point runs sm_100a CUDA
+ * kernels, and returns DG_E_CUDA when no usable device is present.
+ */
+#ifndef DG_B200_H
+#define DG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes map 1:1 onto the reference's exception types
+ * (proj/include/densegraph/errors.hpp:10-42). */
+typedef enum {
+  DG_OK = 0,
+  DG_E_PARSE = 1,        /* ParseError        errors.hpp:10-15 */
+  DG_E_EMPTY = 2,        /* EmptyGraphError   errors.hpp:17-19 */
+  DG_E_IO = 3,           /* IoError           errors.hpp:21-23 */
+  DG_E_PARAM = 4,        /* ParamError        errors.hpp:25-27 */
+  DG_E_INVARIANT = 5,    /* InvariantError    errors.hpp:30-32 */
+  DG_E_ORACLE_SIZE = 6,  /* OracleSizeError   errors.hpp:35-37 */
+  DG_E_CACHE_HASH = 7,   /* CacheHashError    errors.hpp:40-42 */
+  DG_E_NOMEM = 8,        /* device/host allocation failure (-> InvariantError, CLI exit 4) */
+  DG_E_CUDA = 9          /* CUDA runtime failure / no device (-> InvariantError) */
+} dg_status;
+
+typedef struct dg_graph dg_graph; /* device-resident CSR, graph.hpp:24-45 layout */
+
+/* Thread-local message of the last failing call on this thread. */
+const char* dg_last_error(void);
+/* Library version string, e.g. "densegraph-b200 0.1 sm_100a". */
+const char* dg_version(void);
+
+/* ------------------------------------------------------------ graph / CSR */
+
+/* CSR build with the reference's cleanup semantics: canonical (min,max)
+ * pairs, self-loops dropped, duplicates collapsed, dense ids = rank of the
+ * original id among ids that occur in a non-loop edge, rows ascending.
+ * Replaces the CSR-build half of parse_edge_list (io.hpp:18, io.cpp:51-92).
+ * `on_device` != 0: u, v are device pointers (e.g. from dg_gen_rmat).
+ * DG_E_EMPTY if no edge survives (io.cpp:58). */
+dg_status dg_graph_build(const uint64_t* u, const uint64_t* v, uint64_t k, int on_device,
+                         dg_graph** out);
+
+/* Wrap an existing CSR (Graph{n,m,offs,adj,orig}, graph.hpp:24-30). Copies
+ * host arrays (on_device == 0) or device arrays (on_device != 0). */
+dg_status dg_graph_from_csr(uint64_t n, const uint64_t* offs, const uint32_t* adj,
+                            const uint64_t* orig, int on_device, dg_graph** out);
+
+/* GraphStats (graph.hpp:14-18,37-42). */
+dg_status dg_graph_info(const dg_graph* g, uint64_t* n, uint64_t* m, uint64_t* max_degree);
+
+/* Copy the CSR to host buffers of sizes n+1, 2m, n (any may be NULL). */
+dg_status dg_graph_download(const dg_graph* g, uint64_t* offs, uint32_t* adj, uint64_t* orig);
+
+/* Device pointers of the CSR (valid until dg_graph_free). */
+dg_status dg_graph_device_ptrs(const dg_graph* g, const uint64_t** offs, const uint32_t** adj,
+                               const uint64_t** orig);
+
+void dg_graph_free(dg_graph* g);
+
+/* induced_subgraph(g, keep, &old_to_new)  (graph.hpp:50-80).
+ * keep: n bytes (host), old_to_new: n entries (host, nullable). */
+dg_status dg_induced(const dg_graph* g, const uint8_t* keep, dg_graph** out,
+                     uint32_t* old_to_new);
+
+/* get_core(g, dec, k, &old_to_new)  (core.hpp:31-32, core.cpp:133-140):
+ * subgraph induced by labels >= k.  labels: n entries (host). */
+dg_status dg_get_core(const dg_graph* g, const uint32_t* labels, uint32_t k, dg_graph** out,
+                      uint32_t* old_to_new);
+
+/* ------------------------------------------------------------ coreness */
+
+/* exact_coreness (core.hpp:22, core.cpp:123-125) when approx == 0;
+ * approx_coreness(g, c_num, c_den) (core.hpp:28, core.cpp:127-131) otherwise.
+ * labels: n entries (host, nullable).  DG_E_EMPTY on n == 0,
+ * DG_E_PARAM on c_num/c_den <= 1 (approx). */
+dg_status dg_coreness(const dg_graph* g, int approx, uint64_t c_num, uint64_t c_den,
+                      uint32_t* labels, uint32_t* kmax, uint32_t* peel_rounds);
+
+/* ------------------------------------------------------------ refinement */
+
+typedef struct {
+  uint64_t rho_edges, rho_verts; /* RefineOutcome::rho_max, unreduced (refine.hpp:21) */
+  uint64_t best_prefix;          /* refine.hpp:22 */
+  uint64_t width;                /* refine.hpp:23 */
+} dg_outcome;
+
+/* load_peel_order(g, {loads}, one_at_a_time) (refine.hpp:32, refine.cpp:149-156):
+ * min-key batch peel on key = load + residual degree.  perm: n entries. */
+dg_status dg_peel_order(const dg_graph* g, const uint64_t* loads, int one_at_a_time,
+                        uint32_t* perm);
+
+/* load_sort_order({loads}) (refine.hpp:35, refine.cpp:158-178): stable sort by (load, id). */
+dg_status dg_sort_order(uint64_t n, const uint64_t* loads, uint32_t* perm);
+
+/* density_and_load_update(g, order, state, want_densities) (refine.hpp:40-41,
+ * refine.cpp:180-220).  loads updated in place.  suffix_edges (nullable,
+ * n entries): the per-position densities' numerators (denominator n - i).
+ * DG_E_INVARIANT if perm is not a permutation (refine.cpp:186-192). */
+dg_status dg_density_load_update(const dg_graph* g, const uint32_t* perm, uint64_t* loads,
+                                 dg_outcome* out, uint64_t* suffix_edges);
+
+/* charikar_peel (refine.hpp:44, refine.cpp:222-227). */
+dg_status dg_charikar_peel(const dg_graph* g, dg_outcome* out);
+
+/* slack_violations (refine.hpp:48-49, refine.cpp:229-242). */
+dg_status dg_slack_violations(uint64_t n, const uint32_t* perm, const uint64_t* loads,
+                              uint64_t allowed_slack, uint64_t samples, uint64_t seed,
+                              uint64_t* violations);
+
+/* default_iterations (framework.hpp:63, framework.cpp:36-44). Host scalar math. */
+dg_status dg_default_iterations(uint64_t delta, double lower_bound, uint64_t n, double epsilon,
+                                uint64_t cap, uint64_t* out);
+
+/* ------------------------------------------------------------ framework */
+
+typedef struct { /* RunConfig, framework.hpp:15-25 (threads has no meaning here) */
+  int algorithm;         /* 0 peel (Greedy++), 1 sort (GreedySorting++) */
+  int pruning;           /* 0 none, 1 exact, 2 approx, 3 hybrid */
+  uint64_t iterations;   /* explicit T; 0 defers to epsilon */
+  double epsilon;
+  uint64_t iteration_cap;
+  uint64_t c_num, c_den;
+  int reset_loads;
+  uint64_t slack_samples;
+} dg_run_config;
+
+typedef struct { /* IterRecord (framework.hpp:27-33) + device timings */
+  uint64_t iter, rho_edges, rho_verts, n, m, width;
+  double ms;          /* ordering + audit + Alg. 3, CUDA events */
+  double order_ms;    /* ordering kernel alone */
+  double update_ms;   /* Alg. 3 kernels alone */
+  uint64_t batches;   /* Greedy++ batches in this ordering (0 for sort) */
+} dg_iter_record;
+
+typedef struct { /* RunResult + RunTrace/InitRecord (framework.hpp:35-60) */
+  uint64_t best_edges, best_verts; /* reduced */
+  uint64_t witness_size, witness_edges, iterations, max_width;
+  uint64_t slack_violations;
+  int kmax_known, kmax_exact;
+  uint32_t kmax, threshold;
+  uint64_t pruned_n, pruned_m;
+  uint64_t final_n;
+  uint32_t peel_rounds;  /* of the (first) coreness pass */
+  uint32_t reprunes;
+  double coreness_ms;    /* InitRecord::coreness_ms: coreness + get_core + remap */
+  double coreness_kernel_ms; /* the k-core kernel alone */
+  double init_ms, total_ms;
+  double reprune_ms;     /* all mid-run re-prune compactions */
+} dg_run_result;
+
+/* run(g, cfg) (framework.hpp:68, framework.cpp:46-180): Algorithm 1 on the
+ * device; only scalars cross PCIe per iteration.  trace: trace_cap records;
+ * witness: original ids ascending (witness_cap); final_ids: original ids of
+ * the last pruned graph (final_cap).  Any of the arrays may be NULL. */
+dg_status dg_run(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
+                 dg_iter_record* trace, uint64_t trace_cap, uint64_t* witness,
+                 uint64_t witness_cap, uint64_t* final_ids, uint64_t final_cap);
+
+/* ------------------------------------------------------------ synthetic inputs */
+
+/* Seeded counter-based generators (bit-identical to oracle/dg_oracle.c).
+ * Outputs are device buffers allocated with dg_device_alloc when
+ * on_device != 0, else host buffers of `samples` / `pairs` entries. */
+dg_status dg_gen_rmat(uint32_t scale, uint64_t samples, uint64_t seed, uint64_t* u, uint64_t* v,
+                      int on_device);
+dg_status dg_gen_chung_lu(uint64_t n, uint64_t pairs, double n_root11, uint64_t seed,
+                          uint64_t* u, uint64_t* v, int on_device);
+
+/* Device memory helpers for callers that keep inputs resident in HBM. */
+dg_status dg_device_alloc(uint64_t bytes, void** ptr);
+dg_status dg_device_free(void* ptr);
+dg_status dg_memcpy(void* dst, const void* src, uint64_t bytes, int kind /* 1 h2d, 2 d2h, 3 d2d */);
+dg_status dg_synchronize(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,242 @@
+// common.cuh -- shared plumbing for the densegraph B200 library:
+// status/exception mapping, the library stream, stream-ordered device
+// buffers, splitmix64, exact 128-bit density compare, block scans and the
+// grid barrier used by the persistent kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "dg_b200.h"
+
+namespace dgb {
+
+constexpr uint32_t kNoVertex = 0xffffffffu;  // graph.hpp:12
+
+struct DgError : std::runtime_error {
+  dg_status code;
+  DgError(dg_status c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+[[noreturn]] inline void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+           cudaGetErrorString(e), what, file, line);
+  if (e == cudaErrorMemoryAllocation) throw DgError(DG_E_NOMEM, buf);
+  throw DgError(DG_E_CUDA, buf);
+}
+
+#define DG_CUDA(call)                                                  \
+  do {                                                                 \
+    cudaError_t e_ = (call);                                           \
+    if (e_ != cudaSuccess) ::dgb::throw_cuda(e_, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define DG_CHECK_LAUNCH() DG_CUDA(cudaGetLastError())
+
+// The library's stream on the current device (one per device, created
+// lazily).  Every entry point enqueues on it and synchronises before
+// returning, so calls are externally synchronous like the reference's.
+cudaStream_t stream();
+int num_sms();
+void stream_sync();
+
+// Stream-ordered device buffer (cudaMallocAsync on the library stream).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, n = o.n;
+      o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) DG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream()));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, stream());
+    p = nullptr, n = 0;
+  }
+  void zero() {
+    if (n) DG_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), stream()));
+  }
+  void fill_ff() {
+    if (n) DG_CUDA(cudaMemsetAsync(p, 0xff, n * sizeof(T), stream()));
+  }
+  T* get() const { return p; }
+};
+
+template <class T>
+inline void h2d(T* dst, const T* src, size_t count) {
+  if (count) DG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, stream()));
+}
+template <class T>
+inline void d2h(T* dst, const T* src, size_t count) {
+  if (count) DG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, stream()));
+}
+template <class T>
+inline void d2d(T* dst, const T* src, size_t count) {
+  if (count)
+    DG_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToDevice, stream()));
+}
+template <class T>
+inline T read_scalar(const T* dptr) {
+  T v;
+  DG_CUDA(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, stream()));
+  stream_sync();
+  return v;
+}
+
+inline unsigned grid_for(uint64_t work, unsigned block, unsigned cap_per_sm = 8) {
+  uint64_t g = (work + block - 1) / block;
+  uint64_t cap = uint64_t(num_sms()) * cap_per_sm;
+  if (g > cap) g = cap;
+  return g ? unsigned(g) : 1u;
+}
+
+// ------------------------------------------------------------------ device helpers
+
+// splitmix64 (reference parallel.hpp:92-97)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// Exact Density compare a_e/a_v > b_e/b_v by 128-bit cross products
+// (reference density.hpp:32-36).
+__device__ __forceinline__ bool dens_gt(uint64_t ae, uint64_t av, uint64_t be, uint64_t bv) {
+  uint64_t lhs_hi = __umul64hi(ae, bv), lhs_lo = ae * bv;
+  uint64_t rhs_hi = __umul64hi(be, av), rhs_lo = be * av;
+  return lhs_hi > rhs_hi || (lhs_hi == rhs_hi && lhs_lo > rhs_lo);
+}
+__device__ __forceinline__ bool dens_ge(uint64_t ae, uint64_t av, uint64_t be, uint64_t bv) {
+  return !dens_gt(be, bv, ae, av);
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T x) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane_id() >= (unsigned)o) x += y;
+  }
+  return x;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_min(T x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    T y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y < x ? y : x;
+  }
+  return x;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_max(T x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    T y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y > x ? y : x;
+  }
+  return x;
+}
+
+// Block-wide exclusive scan of one value per thread; every thread calls it.
+// `ws` is __shared__ scratch of >= 33 elements.  Returns the exclusive
+// prefix; *total receives the block total.  Two __syncthreads.
+template <class T>
+__device__ __forceinline__ T block_excl_scan(T x, T* ws, T* total) {
+  const unsigned w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  T inc = warp_incl_scan(x);
+  if (lane_id() == 31) ws[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T v = lane_id() < nw ? ws[lane_id()] : T(0);
+    T vi = warp_incl_scan(v);
+    ws[lane_id()] = vi - v;
+    if (lane_id() == 31) ws[32] = vi;
+  }
+  __syncthreads();
+  T r = ws[w] + inc - x;
+  *total = ws[32];
+  return r;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Sense-free generation barrier for a co-resident (cooperatively launched)
+// grid.  Thread 0 of each CTA arrives with a release-ordered atomic and
+// spins on the generation word with acquire loads.  A spin that exceeds
+// `timeout_cycles` raises *abort (the kernel then unwinds instead of
+// hanging the device).
+struct GridBarrier {
+  uint32_t count;
+  uint32_t gen;
+  uint32_t abort;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ bool grid_sync(GridBarrier* b, uint32_t nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t g = ld_acquire_u32(&b->gen);
+    __threadfence();
+    uint32_t arrived = atomicAdd(&b->count, 1u);
+    if (arrived == nblocks - 1) {
+      __threadfence();
+      b->count = 0;
+      st_release_u32(&b->gen, g + 1);
+    } else {
+      long long t0 = clock64();
+      while (ld_acquire_u32(&b->gen) == g) {
+        if (ld_acquire_u32(&b->abort)) break;
+        if (clock64() - t0 > (1LL << 33)) {  // ~4 s at 2 GHz
+          atomicExch(&b->abort, 1u);
+          break;
+        }
+      }
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return *(volatile uint32_t*)&b->abort == 0;
+}
+
+}  // namespace dgb

@@ -1,0 +1,477 @@
+// peel.cu -- Greedy++ ordering and Algorithm 3 (reference refine.cpp).
+//
+// k_peel: the whole min-key batch chain of one iteration in ONE CTA
+// (refine.cpp:20-156 semantics).  Keys (load - base + residual degree) live
+// in shared memory when they fit (u32 keys when the key range allows, u64
+// otherwise), so every batch is: CTA-wide min + ordered batch extraction
+// (one barrier: warp min/count -> warp table -> every warp re-reduces the 32
+// entries), then a load-balanced pass over the batch's adjacency lists that
+// decrements alive neighbours' keys with shared-memory atomics and, fused,
+// counts Algorithm 3's charge A[pos(v)] (= alive neighbours after v's batch
+// + same-batch neighbours with a larger id, refine.cpp:195-199).  No host
+// round trip and no global barrier per batch.
+//
+// k_alg3: suffix sums of A, first strict argmax of B[i]/(n-i) with exact
+// 128-bit compares, width = max A, loads += A, the sampled slack audit on the
+// pre-update loads, and the next iteration's key range -- one CTA.
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace dgb {
+
+namespace {
+
+constexpr int PT = 1024;  // peel CTA size
+constexpr size_t kSmemCap = 227 * 1024;
+
+template <class K>
+struct PeelArgs {
+  const uint64_t* offs;
+  const uint32_t* adj;
+  uint32_t n;
+  const uint64_t* loads;
+  uint64_t base;
+  int one;
+  K* gkeys;
+  uint32_t chunk;
+  uint32_t* perm;
+  uint32_t* charges;
+  unsigned long long* batches;
+};
+
+struct PeelSmem {  // fixed part, after the keys
+  uint32_t v[PT];
+  uint64_t off[PT];
+  uint64_t pre[PT];
+  uint32_t cnt[PT];
+  uint64_t ws[33];
+  uint64_t wmin[32];
+  uint32_t wcnt[32];
+};
+
+template <class K>
+__device__ __forceinline__ void key_dec(K* p);
+template <>
+__device__ __forceinline__ void key_dec<uint32_t>(uint32_t* p) {
+  atomicSub(p, 1u);
+}
+template <>
+__device__ __forceinline__ void key_dec<uint64_t>(uint64_t* p) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), ~0ULL);
+}
+
+template <class K, bool SMEM>
+__global__ void __launch_bounds__(PT, 1) k_peel(PeelArgs<K> a) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  const uint32_t npad = a.chunk * PT;
+  K* keys = SMEM ? reinterpret_cast<K*>(raw) : a.gkeys;
+  PeelSmem& s = *reinterpret_cast<PeelSmem*>(
+      raw + (SMEM ? ((size_t(npad) * sizeof(K) + 15) & ~size_t(15)) : 0));
+  const K DEAD = K(~K(0)), BATCH = K(DEAD - 1);
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
+  const uint32_t n = a.n, c = a.chunk, lo = tid * c, hi = lo + c;
+
+  for (uint32_t i = lo; i < hi; ++i)
+    keys[i] = i < n ? K(a.loads[i] - a.base + (a.offs[i + 1] - a.offs[i])) : DEAD;
+  __syncthreads();
+
+  uint32_t removed = 0, pos = 0;
+  unsigned long long nbat = 0;
+  while (removed < n) {
+    // ---- S1: per-thread min over its chunk (old batch marks -> DEAD)
+    K lmin = DEAD;
+    uint32_t lcnt = 0;
+    for (uint32_t i = lo; i < hi; ++i) {
+      K k = keys[i];
+      if (k >= BATCH) {
+        if (k == BATCH) keys[i] = DEAD;
+        continue;
+      }
+      if (k < lmin) {
+        lmin = k;
+        lcnt = 1;
+      } else if (k == lmin) {
+        ++lcnt;
+      }
+    }
+    const K wm = warp_min(lmin);
+    const uint32_t contrib = (lmin == wm) ? lcnt : 0u;
+    const uint32_t incl = warp_incl_scan(contrib);
+    if (lane == 31) {
+      s.wmin[w] = uint64_t(wm);
+      s.wcnt[w] = incl;
+    }
+    __syncthreads();
+    // every warp reduces the 32 warp entries itself (no second barrier)
+    const K x = K(s.wmin[lane]);
+    const K gmin = warp_min(x);
+    const uint32_t cc = (x == gmin) ? s.wcnt[lane] : 0u;
+    const uint32_t ci = warp_incl_scan(cc);
+    const uint32_t total = __shfl_sync(0xffffffffu, ci, 31);
+    const uint32_t woff = __shfl_sync(0xffffffffu, ci - cc, w);
+    const uint32_t bs = a.one ? 1u : total;
+    // ---- S2: the batch in ascending id, straight into perm
+    if (lmin == gmin && lcnt) {
+      uint32_t my = woff + incl - contrib;
+      for (uint32_t i = lo; i < hi && my < bs; ++i)
+        if (keys[i] == gmin) {
+          a.perm[pos + my] = i;
+          keys[i] = BATCH;
+          ++my;
+        }
+    }
+    __syncthreads();
+    // ---- S3: remove the batch, slice by slice
+    for (uint32_t s0 = 0; s0 < bs; s0 += PT) {
+      const uint32_t sl = min(uint32_t(PT), bs - s0);
+      uint64_t d = 0;
+      if (tid < sl) {
+        const uint32_t v = a.perm[pos + s0 + tid];
+        const uint64_t o = a.offs[v];
+        d = a.offs[v + 1] - o;
+        s.v[tid] = v;
+        s.off[tid] = o;
+        s.cnt[tid] = 0;
+      }
+      uint64_t tot;
+      const uint64_t ex = block_excl_scan(d, s.ws, &tot);
+      s.pre[tid] = ex + d;  // inclusive
+      __syncthreads();
+      for (uint64_t b0 = tid & ~31u; b0 < tot; b0 += PT) {
+        const uint64_t x2 = b0 + lane;
+        const bool valid = x2 < tot;
+        uint32_t b = 0, cnt = 0;
+        if (valid) {
+          uint32_t l = 0, h = sl - 1;  // first b with pre[b] > x2
+          while (l < h) {
+            uint32_t mid = (l + h) >> 1;
+            if (s.pre[mid] > x2)
+              h = mid;
+            else
+              l = mid + 1;
+          }
+          b = l;
+          const uint32_t v = s.v[b];
+          const uint32_t u = a.adj[s.off[b] + (x2 - (b ? s.pre[b - 1] : 0))];
+          const K k = keys[u];
+          if (k < BATCH) {
+            key_dec<K>(&keys[u]);
+            cnt = 1;
+          } else if (k == BATCH && u > v) {
+            cnt = 1;
+          }
+        }
+        const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+          const uint32_t grp = __match_any_sync(vm, b);
+          const uint32_t sum = __popc(__ballot_sync(vm, cnt) & grp);
+          if (lane == uint32_t(__ffs(grp) - 1) && sum) atomicAdd(&s.cnt[b], sum);
+        }
+      }
+      __syncthreads();
+      if (tid < sl) a.charges[pos + s0 + tid] = s.cnt[tid];
+      __syncthreads();
+    }
+    pos += bs;
+    removed += bs;
+    ++nbat;
+  }
+  if (tid == 0) *a.batches = nbat;
+}
+
+// ---- key range: min load, max (load - min + deg)
+__global__ void k_key_range(const uint64_t* offs, const uint64_t* loads, uint64_t n,
+                            unsigned long long* mn, unsigned long long* mx) {
+  uint64_t lmin = ~0ULL;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    lmin = min(lmin, loads[i]);
+  lmin = warp_min(lmin);
+  if (lane_id() == 0) atomicMin(mn, (unsigned long long)lmin);
+}
+__global__ void k_key_max(const uint64_t* offs, const uint64_t* loads, uint64_t n,
+                          const unsigned long long* mn, unsigned long long* mx) {
+  const uint64_t base = *mn;
+  uint64_t lmax = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    lmax = max(lmax, loads[i] - base + (offs[i + 1] - offs[i]));
+  lmax = warp_max(lmax);
+  if (lane_id() == 0) atomicMax(mx, (unsigned long long)lmax);
+}
+
+// ---- Algorithm 3 ----
+struct A3Args {
+  const uint64_t* offs;
+  uint32_t n;
+  const uint32_t* perm;
+  const uint32_t* A;
+  uint64_t* loads;
+  uint64_t slack_samples, slack_allowed, slack_seed;
+  uint64_t* suffix;
+  Alg3Out* out;
+};
+
+__device__ __forceinline__ bool better(uint64_t e1, uint64_t v1, uint64_t i1, uint64_t e2,
+                                       uint64_t v2, uint64_t i2) {
+  // strictly denser, or equally dense at a smaller position
+  if (dens_gt(e1, v1, e2, v2)) return true;
+  if (dens_gt(e2, v2, e1, v1)) return false;
+  return i1 < i2;
+}
+
+__global__ void __launch_bounds__(PT, 1) k_alg3(A3Args a) {
+  __shared__ uint64_t ws[33];
+  __shared__ uint64_t r_e[32], r_v[32], r_i[32], r_w[32], r_x[32], r_y[32];
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5, nw = blockDim.x >> 5;
+  const uint32_t n = a.n;
+  // slack audit on the pre-update loads (refine.cpp:229-242)
+  uint64_t bad = 0;
+  if (n >= 2)
+    for (uint64_t t = tid; t < a.slack_samples; t += blockDim.x) {
+      uint64_t i = mix64(a.slack_seed ^ (2 * t + 1)) % n;
+      uint64_t j = mix64(a.slack_seed ^ (2 * t + 2)) % n;
+      if (i == j) continue;
+      if (i > j) {
+        uint64_t s = i;
+        i = j;
+        j = s;
+      }
+      if (a.loads[a.perm[i]] > a.loads[a.perm[j]] + a.slack_allowed) ++bad;
+    }
+  uint64_t badsum;
+  block_excl_scan(bad, ws, &badsum);
+
+  // chunked suffix sums
+  const uint32_t c = (n + blockDim.x - 1) / blockDim.x;
+  const uint32_t lo = min(n, tid * c), hi = min(n, lo + c);
+  uint64_t local = 0;
+  uint32_t wmax = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const uint32_t x = a.A[i];
+    local += x;
+    wmax = max(wmax, x);
+  }
+  uint64_t total;
+  const uint64_t ex = block_excl_scan(local, ws, &total);
+  uint64_t run = total - ex - local;  // sum of A beyond my chunk
+  uint64_t be = 0, bv = 1, bi = ~0ULL;
+  for (uint32_t i = hi; i-- > lo;) {
+    run += a.A[i];
+    if (a.suffix) a.suffix[i] = run;
+    const uint64_t d = n - i;
+    if (!dens_gt(be, bv, run, d)) {  // >= : walking down, smaller i wins ties
+      be = run;
+      bv = d;
+      bi = i;
+    }
+  }
+  // block argmax (tie -> smaller position), width
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    uint64_t e2 = __shfl_xor_sync(0xffffffffu, be, o);
+    uint64_t v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    uint64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(e2, v2, i2, be, bv, bi)) be = e2, bv = v2, bi = i2;
+  }
+  wmax = warp_max(wmax);
+  if (lane == 0) r_e[w] = be, r_v[w] = bv, r_i[w] = bi, r_w[w] = wmax;
+  __syncthreads();
+  if (w == 0) {
+    be = lane < nw ? r_e[lane] : 0;
+    bv = lane < nw ? r_v[lane] : 1;
+    bi = lane < nw ? r_i[lane] : ~0ULL;
+    uint64_t wm = lane < nw ? r_w[lane] : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      uint64_t e2 = __shfl_xor_sync(0xffffffffu, be, o);
+      uint64_t v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      uint64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(e2, v2, i2, be, bv, bi)) be = e2, bv = v2, bi = i2;
+    }
+    wm = warp_max(wm);
+    if (lane == 0) {
+      if (be == 0) {  // every suffix has density 0: rho stays {0,1} at prefix 0
+        a.out->rho_edges = 0;
+        a.out->rho_verts = 1;
+        a.out->best_prefix = 0;
+      } else {
+        a.out->rho_edges = be;
+        a.out->rho_verts = bv;
+        a.out->best_prefix = bi;
+      }
+      a.out->width = wm;
+      a.out->total = total;
+      a.out->slack_bad = badsum;
+    }
+  }
+  // loads += A (refine.cpp:213)
+  for (uint32_t i = lo; i < hi; ++i) a.loads[a.perm[i]] += a.A[i];
+  __syncthreads();
+  // next key range over vertices
+  uint64_t mn = ~0ULL;
+  for (uint32_t v = tid; v < n; v += blockDim.x) mn = min(mn, a.loads[v]);
+  mn = warp_min(mn);
+  if (lane == 0) r_x[w] = mn;
+  __syncthreads();
+  if (w == 0) {
+    uint64_t x = lane < nw ? r_x[lane] : ~0ULL;
+    x = warp_min(x);
+    if (lane == 0) r_x[0] = x;
+  }
+  __syncthreads();
+  const uint64_t base = r_x[0];
+  uint64_t mk = 0;
+  for (uint32_t v = tid; v < n; v += blockDim.x)
+    mk = max(mk, a.loads[v] - base + (a.offs[v + 1] - a.offs[v]));
+  mk = warp_max(mk);
+  if (lane == 0) r_y[w] = mk;
+  __syncthreads();
+  if (w == 0) {
+    uint64_t x = lane < nw ? r_y[lane] : 0;
+    x = warp_max(x);
+    if (lane == 0) {
+      a.out->min_load = n ? base : 0;
+      a.out->max_key = x;
+    }
+  }
+}
+
+// ---- charges from an arbitrary permutation (refine.cpp:186-199)
+__global__ void k_pos_from_perm(const uint32_t* perm, uint64_t n, uint64_t* pos, uint32_t* err) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = perm[i];
+    if (v >= n) {
+      *err = 1;
+      continue;
+    }
+    unsigned long long old =
+        atomicCAS(reinterpret_cast<unsigned long long*>(&pos[v]), ~0ULL, (unsigned long long)i);
+    if (old != ~0ULL) *err = 1;
+  }
+}
+
+__global__ void k_charges(const uint64_t* offs, const uint32_t* adj, uint64_t n,
+                          const uint64_t* pos, uint32_t* A) {
+  const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t v = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; v < n; v += warps) {
+    const uint64_t pv = pos[v];
+    for (uint64_t p = offs[v] + lane_id(); p < offs[v + 1]; p += 32) {
+      const uint32_t u = adj[p];
+      if (u > v) atomicAdd(&A[min(pv, pos[u])], 1u);
+    }
+  }
+}
+
+__global__ void k_iota(uint32_t* p, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    p[i] = uint32_t(i);
+}
+
+template <class K, bool SMEM>
+void launch_peel(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
+                 uint32_t chunk, uint32_t* d_perm, uint32_t* d_charges,
+                 unsigned long long* d_batches) {
+  DevBuf<K> gk;
+  size_t smem = sizeof(PeelSmem);
+  if (SMEM)
+    smem += (size_t(chunk) * PT * sizeof(K) + 15) & ~size_t(15);
+  else
+    gk.alloc(size_t(chunk) * PT);
+  DG_CUDA(cudaFuncSetAttribute(k_peel<K, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  PeelArgs<K> a{g.offs.get(), g.adj.get(), uint32_t(g.n), d_loads, base, one ? 1 : 0,
+                gk.get(), chunk, d_perm, d_charges, d_batches};
+  k_peel<K, SMEM><<<1, PT, smem, stream()>>>(a);
+  DG_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+KeyRange key_range(const dg_graph& g, const uint64_t* d_loads) {
+  KeyRange kr;
+  if (!g.n) return kr;
+  DevBuf<unsigned long long> mm(2);
+  unsigned long long init[2] = {~0ULL, 0ULL};
+  h2d(mm.get(), init, 2);
+  k_key_range<<<grid_for(g.n, 256), 256, 0, stream()>>>(g.offs.get(), d_loads, g.n, mm.get(),
+                                                        mm.get() + 1);
+  DG_CHECK_LAUNCH();
+  k_key_max<<<grid_for(g.n, 256), 256, 0, stream()>>>(g.offs.get(), d_loads, g.n, mm.get(),
+                                                      mm.get() + 1);
+  DG_CHECK_LAUNCH();
+  unsigned long long h[2];
+  d2h(h, mm.get(), 2);
+  stream_sync();
+  kr.min_load = h[0];
+  kr.max_key = h[1];
+  return kr;
+}
+
+void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
+                bool one_at_a_time, uint32_t* d_perm, uint32_t* d_charges,
+                unsigned long long* d_batches) {
+  if (g.n == 0) return;
+  const uint32_t n = uint32_t(g.n);
+  uint32_t chunk = (n + PT - 1) / PT;
+  chunk |= 1u;  // odd stride: conflict-free shared-memory chunk scans
+  unsigned long long* nb = d_batches;
+  const size_t fixed = sizeof(PeelSmem) + 16;
+  const bool k32 = kr.max_key < 0xfffffffdULL;
+  if (k32 && fixed + size_t(chunk) * PT * 4 <= kSmemCap)
+    launch_peel<uint32_t, true>(g, d_loads, kr.min_load, one_at_a_time, chunk, d_perm, d_charges,
+                                nb);
+  else if (!k32 && fixed + size_t(chunk) * PT * 8 <= kSmemCap)
+    launch_peel<uint64_t, true>(g, d_loads, kr.min_load, one_at_a_time, chunk, d_perm, d_charges,
+                                nb);
+  else if (k32)
+    launch_peel<uint32_t, false>(g, d_loads, kr.min_load, one_at_a_time, chunk, d_perm,
+                                 d_charges, nb);
+  else
+    launch_peel<uint64_t, false>(g, d_loads, kr.min_load, one_at_a_time, chunk, d_perm,
+                                 d_charges, nb);
+}
+
+void sort_order(uint64_t n, const uint64_t* d_loads, uint32_t* d_perm) {
+  if (!n) return;
+  DevBuf<uint32_t> ids(n);
+  DevBuf<uint64_t> ksorted(n);
+  k_iota<<<grid_for(n, 256), 256, 0, stream()>>>(ids.get(), n);
+  DG_CHECK_LAUNCH();
+  size_t tmp = 0;
+  DG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, d_loads, ksorted.get(), ids.get(), d_perm,
+                                          n, 0, 64, stream()));
+  DevBuf<char> t(tmp);
+  DG_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, d_loads, ksorted.get(), ids.get(),
+                                          d_perm, n, 0, 64, stream()));
+}
+
+void charges_from_perm(const dg_graph& g, const uint32_t* d_perm, uint32_t* d_charges) {
+  const uint64_t n = g.n;
+  if (!n) return;
+  DevBuf<uint64_t> pos(n);
+  pos.fill_ff();
+  DevBuf<uint32_t> err(1);
+  err.zero();
+  k_pos_from_perm<<<grid_for(n, 256), 256, 0, stream()>>>(d_perm, n, pos.get(), err.get());
+  DG_CHECK_LAUNCH();
+  if (read_scalar(err.get())) throw DgError(DG_E_INVARIANT, "ordering is not a permutation");
+  DG_CUDA(cudaMemsetAsync(d_charges, 0, n * sizeof(uint32_t), stream()));
+  k_charges<<<grid_for(n * 32, 256), 256, 0, stream()>>>(g.offs.get(), g.adj.get(), n, pos.get(),
+                                                         d_charges);
+  DG_CHECK_LAUNCH();
+}
+
+void alg3(const dg_graph& g, const uint32_t* d_perm, const uint32_t* d_charges, uint64_t* d_loads,
+          uint64_t slack_samples, uint64_t slack_allowed, uint64_t slack_seed, uint64_t* d_suffix,
+          Alg3Out* d_out) {
+  A3Args a{g.offs.get(), uint32_t(g.n), d_perm, d_charges, d_loads, slack_samples, slack_allowed,
+           slack_seed, d_suffix, d_out};
+  k_alg3<<<1, PT, 0, stream()>>>(a);
+  DG_CHECK_LAUNCH();
+}
+
+}  // namespace dgb

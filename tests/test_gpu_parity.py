@@ -1,0 +1,314 @@
+"""GPU parity: the CUDA path through the C ABI against the golden fixtures
+(produced by the unmodified reference) and the pinned CPU oracle.
+
+Everything integer is compared bit-exactly: CSR arrays, core labels, kmax,
+peel_rounds, Greedy++ permutations (batch and one-at-a-time), per-iteration
+loads, suffix densities, widths, run traces, witnesses, final vertex sets.
+"""
+import hashlib
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import graphs as G
+from oracle import RunConfig as ORunConfig, gnp_edges, mix64, random_loads
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+def dgraph(dg, edges):
+    u, v = G.uv(edges)
+    return dg.Graph.from_pairs(u, v)
+
+
+def same_csr(g, h):
+    return (np.array_equal(g.offs, h.offs) and np.array_equal(g.adj, h.adj)
+            and np.array_equal(g.orig, h.orig))
+
+
+# ------------------------------------------------------------------ CSR build
+def test_build_cleanup_rules(dg):
+    g = dg.Graph.from_pairs(np.array([0, 1, 3, 7], np.uint64), np.array([1, 0, 3, 5], np.uint64))
+    assert (g.n, g.m) == (4, 2)
+    assert g.orig.tolist() == [0, 1, 5, 7] and g.adj.tolist() == [1, 0, 3, 2]
+    with pytest.raises(dg.EmptyGraphError):
+        dg.Graph.from_pairs(np.array([3, 4], np.uint64), np.array([3, 4], np.uint64))
+    with pytest.raises(dg.EmptyGraphError):
+        dg.Graph.from_pairs(np.array([], np.uint64), np.array([], np.uint64))
+
+
+@pytest.mark.parametrize("seed", range(1, 9))
+def test_build_matches_oracle_gnp(dg, orc, seed):
+    n = 2 + mix64(seed) % 150
+    u, v = orc.gen_gnp(n, 20 + seed * 97 % 600, seed)
+    assert same_csr(dg.Graph.from_pairs(u, v), orc.build(u, v))
+
+
+def test_build_sparse_64bit_ids(dg, orc):
+    """ids above 2^32 take the sort + binary-search relabel path."""
+    rng = np.random.default_rng(5)
+    ids = np.unique(rng.integers(0, 2**62, 3000, dtype=np.uint64))
+    u = ids[rng.integers(0, len(ids), 20000)]
+    v = ids[rng.integers(0, len(ids), 20000)]
+    u[:50] = v[:50]  # self loops
+    assert same_csr(dg.Graph.from_pairs(u, v), orc.build(u, v))
+
+
+def test_build_rmat_and_generators(dg, orc):
+    for scale, seed in ((10, 1), (14, 9)):
+        du, dv = dg.gen_rmat(scale, 16 << scale, seed)
+        hu, hv = orc.gen_rmat(scale, 16 << scale, seed)
+        assert np.array_equal(du, hu) and np.array_equal(dv, hv)
+        assert same_csr(dg.Graph.from_pairs(du, dv), orc.build(hu, hv))
+    du, dv = dg.gen_chung_lu(200000, 400000, 50)
+    hu, hv = orc.gen_chung_lu(200000, 400000, 50)
+    assert np.array_equal(du, hu) and np.array_equal(dv, hv)
+
+
+def test_from_csr_roundtrip(dg, orc):
+    h = orc.build(*orc.gen_rmat(12, 16 << 12, 3))
+    g = dg.Graph.from_csr(h.offs, h.adj, h.orig)
+    assert same_csr(g, h) and g.stats().max_degree == h.max_degree()
+
+
+# ------------------------------------------------------------------ coreness
+def test_coreness_pinned(dg):
+    d = dg.exact_coreness(dgraph(dg, G.clique(5)))
+    assert d.labels.tolist() == [4] * 5 and d.kmax == 4 and d.peel_rounds >= 1
+    assert dg.exact_coreness(dgraph(dg, G.triangle_pendant())).labels.tolist() == [2, 2, 2, 1]
+    assert dg.exact_coreness(dgraph(dg, G.path_graph(4))).labels.tolist() == [1] * 4
+    assert dg.approx_coreness(dgraph(dg, G.path_graph(4)), 3, 2).labels.tolist() == [1] * 4
+    star = dg.exact_coreness(dgraph(dg, G.star(3000)))
+    assert np.all(star.labels == 1) and star.kmax == 1
+    with pytest.raises(dg.ParamError):
+        dg.approx_coreness(dgraph(dg, G.clique(4)), 2, 3)
+
+
+def test_coreness_golden(dg, orc, golden):
+    for c in golden["coreness"]:
+        g = dg.Graph.from_pairs(*orc.gen_gnp(c["n"], c["permille"], c["seed"]))
+        d = dg.exact_coreness(g)
+        assert (d.labels.tolist(), d.kmax, d.peel_rounds) == (c["labels"], c["kmax"], c["rounds"])
+        for cn, cd in ((3, 2), (2, 1), (11, 10)):
+            a = c[f"approx_{cn}_{cd}"]
+            x = dg.approx_coreness(g, cn, cd)
+            assert (x.labels.tolist(), x.kmax, x.peel_rounds) == (a["labels"], a["kmax"], a["rounds"])
+
+
+def test_get_core_pinned(dg):
+    g = dgraph(dg, G.triangle_pendant())
+    c, m = dg.get_core(g, dg.exact_coreness(g), 2, old_to_new=True)
+    assert (c.n, c.m) == (3, 3) and c.orig.tolist() == [0, 1, 2] and m[3] == dg.kNoVertex
+    k, m = dg.induced_subgraph(dgraph(dg, G.clique(4)), [1, 1, 1, 1], old_to_new=True)
+    assert (k.n, k.m) == (4, 6) and m.tolist() == [0, 1, 2, 3]
+    e = dg.induced_subgraph(dgraph(dg, G.clique(4)), [0, 0, 0, 0])
+    assert (e.n, e.m) == (0, 0)
+
+
+def test_induced_matches_oracle_random_masks(dg, orc):
+    h = orc.build(*orc.gen_rmat(13, 16 << 13, 11))
+    g = dg.Graph.from_csr(h.offs, h.adj, h.orig)
+    for s in range(4):
+        keep = (np.arange(h.n) * 2654435761 + s * 97) % (3 + s) == 0
+        a, am = dg.induced_subgraph(g, keep, old_to_new=True)
+        b, bm = orc.induced(h, keep)
+        assert same_csr(a, b) and np.array_equal(am, bm)
+
+
+# ------------------------------------------------------------------ refinement
+def test_peel_pinned(dg):
+    assert dg.load_peel_order(dgraph(dg, G.path_graph(3)), np.zeros(3, np.uint64)).perm.tolist() == [0, 2, 1]
+    assert dg.load_peel_order(dgraph(dg, G.clique(4)), np.zeros(4, np.uint64)).perm.tolist() == [0, 1, 2, 3]
+    loads = np.array([0, 0, 0, 10], np.uint64)
+    assert dg.load_peel_order(dgraph(dg, G.triangle_pendant()), loads).perm.tolist() == [0, 1, 2, 3]
+    assert dg.load_sort_order(np.array([5, 2, 7, 2], np.uint64)).perm.tolist() == [1, 3, 0, 2]
+
+
+def test_peel_golden(dg, orc, golden):
+    for c in golden["peel"]:
+        g = dg.Graph.from_pairs(*orc.gen_gnp(c["n"], c["permille"], c["seed"]))
+        loads = random_loads(g.n, c["loads_maxload"], c["loads_seed"])
+        assert dg.load_peel_order(g, loads).perm.tolist() == c["perm"]
+        assert dg.load_peel_order(g, loads, True).perm.tolist() == c["perm_one"]
+        la = loads.copy()
+        out = dg.density_and_load_update(g, np.array(c["perm"], np.uint32), la, True)
+        assert (out.rho_max.edges, out.rho_max.verts) == tuple(c["rho"])
+        assert out.best_prefix == c["best_prefix"] and out.width == c["width"]
+        assert la.tolist() == c["loads_after"]
+        assert [d.edges for d in out.densities] == c["suffix_edges"]
+
+
+def test_peel_shift_invariance_u64_keys(dg, orc):
+    """loads beyond 2^32 force the 64-bit key path; the order must not change."""
+    for seed in range(1, 6):
+        g = dg.Graph.from_pairs(*G.uv(gnp_edges(60, 80, seed * 11)))
+        small = random_loads(g.n, 9, seed)
+        huge = small + np.uint64(1 << 40)
+        spread = small.copy()
+        spread[0] += np.uint64(1 << 36)  # key range itself beyond 32 bits
+        a = dg.load_peel_order(g, small).perm
+        assert np.array_equal(a, dg.load_peel_order(g, huge).perm)
+        h = orc.build(*G.uv(gnp_edges(60, 80, seed * 11)))
+        assert np.array_equal(dg.load_peel_order(g, spread).perm, orc.peel_order(h, spread))
+
+
+def test_density_golden(dg, orc, golden):
+    for c in golden["density"]:
+        g = dg.Graph.from_pairs(*orc.gen_gnp(c["n"], c["permille"], c["seed"]))
+        loads = random_loads(g.n, c["maxload"], c["loads_seed"])
+        for which in ("peel", "sort"):
+            e = c[which]
+            o = dg.load_peel_order(g, loads) if which == "peel" else dg.load_sort_order(loads)
+            assert o.perm.tolist() == e["perm"]
+            la = loads.copy()
+            out = dg.density_and_load_update(g, o, la, True)
+            assert (out.rho_max.edges, out.rho_max.verts) == tuple(e["rho"])
+            assert out.best_prefix == e["best_prefix"] and out.width == e["width"]
+            assert la.tolist() == e["loads_after"]
+            assert [d.edges for d in out.densities] == e["suffix_edges"]
+
+
+def test_density_contract_errors(dg):
+    g = dgraph(dg, G.clique(3))
+    for perm in ([0, 1, 1], [0, 1, 7]):
+        with pytest.raises(dg.InvariantError):
+            dg.density_and_load_update(g, np.array(perm, np.uint32), np.zeros(3, np.uint64))
+    with pytest.raises(dg.InvariantError):
+        dg.load_peel_order(g, np.zeros(2, np.uint64))
+
+
+def test_charikar_and_slack(dg):
+    assert dg.charikar_peel(dgraph(dg, G.star(5))).rho_max == dg.Density(5, 6)
+    assert dg.charikar_peel(dgraph(dg, G.clique(4))).rho_max == dg.Density(3, 2)
+    assert dg.charikar_peel(dgraph(dg, G.triangle_pendant())).rho_max == dg.Density(1, 1)
+    assert dg.slack_violations(np.arange(6, dtype=np.uint32), np.array([9, 7, 5, 3, 1, 0],
+                                                                       np.uint64), 0, 4000, 1) > 0
+    for seed in range(1, 6):
+        g = dg.Graph.from_pairs(*G.uv(gnp_edges(50, 100, seed * 29)))
+        loads = random_loads(g.n, 20, seed)
+        o = dg.load_peel_order(g, loads)
+        assert dg.slack_violations(o, loads, g.stats().max_degree, 2000, seed) == 0
+
+
+# ------------------------------------------------------------------ framework
+def _graph_for(dg, orc, name):
+    if name == "biclique_k4":
+        return dgraph(dg, G.biclique_with_k4())
+    _, n, p, s = name.split("_")
+    return dg.Graph.from_pairs(*orc.gen_gnp(int(n), int(p), int(s)))
+
+
+def _cmp_run(r, e):
+    assert [r.best.edges, r.best.verts] == e["best"]
+    assert r.witness.tolist() == e["witness"] and r.witness_edges == e["witness_edges"]
+    assert r.iterations == e["iterations"] and r.max_width == e["max_width"]
+    assert r.trace.slack_violations == e["slack_violations"]
+    i = r.trace.init
+    assert (i.kmax_known, i.kmax_exact, i.kmax, i.threshold) == (
+        e["kmax_known"], e["kmax_exact"], e["kmax"], e["threshold"])
+    assert (i.pruned_n, i.pruned_m) == (e["pruned_n"], e["pruned_m"])
+    assert r.trace.final_vertices.tolist() == e["final_vertices"]
+    assert [[t.iter, t.rho.edges, t.rho.verts, t.n, t.m, t.width] for t in r.trace.iters] == e["trace"]
+
+
+def test_run_golden(dg, orc, golden):
+    cache = {}
+    for c in golden["runs"]:
+        g = cache.setdefault(c["graph"], _graph_for(dg, orc, c["graph"]))
+        cfg = dg.RunConfig(algorithm=c["algorithm"], pruning=c["pruning"],
+                           iterations=c["iterations"], reset_loads=c["reset_loads"])
+        _cmp_run(dg.run(g, cfg), c["result"])
+
+
+def test_run_errors(dg):
+    g = dgraph(dg, G.clique(4))
+    with pytest.raises(dg.ParamError):
+        dg.run(g, dg.RunConfig(iterations=0, epsilon=0.0))
+    r = dg.run(g, dg.RunConfig(iterations=0, epsilon=0.9))
+    assert r.iterations >= 10 and len(r.trace.iters) == r.iterations
+
+
+def _synthetic_pairs(orc, s):
+    p = s["params"]
+    if s["kind"] == "rmat":
+        return orc.gen_rmat(p["scale"], p["samples"], p["seed"])
+    if s["kind"] == "er_planted":
+        return orc.gen_er_planted(p["n"], p["m"], p["block"], p["seed"])
+    return orc.gen_chung_lu(p["n"], p["pairs"], p["seed"])
+
+
+def test_synthetic_golden(dg, orc, golden):
+    """RMAT / ER+planted / Chung-Lu fixtures: CSR, labels, core, 5 chained
+    Greedy++ iterations (perm + loads per iteration) and a full run."""
+    for s in golden["synthetic"]:
+        g = dg.Graph.from_pairs(*_synthetic_pairs(orc, s))
+        assert (g.n, g.m) == (s["n"], s["m"])
+        assert (sha(g.offs), sha(g.adj), sha(g.orig)) == (s["offs"], s["adj"], s["orig"])
+        d = dg.exact_coreness(g)
+        assert (sha(d.labels), d.kmax, d.peel_rounds) == (s["labels"], s["kmax"], s["rounds"])
+        core = dg.get_core(g, d, (d.kmax + 1) // 2)
+        assert (core.n, core.m, sha(core.adj), sha(core.orig)) == (
+            s["core_n"], s["core_m"], s["core_adj"], s["core_orig"])
+        loads = np.zeros(core.n, np.uint64)
+        for e in s["core_iters"]:
+            o = dg.load_peel_order(core, loads)
+            out = dg.density_and_load_update(core, o, loads)
+            assert (sha(o.perm), sha(loads)) == (e["perm"], e["loads"])
+            assert [out.rho_max.edges, out.rho_max.verts] == e["rho"] and out.width == e["width"]
+        r = dg.run(g, dg.RunConfig(iterations=s["run_T"]))
+        e = s["run"]
+        assert [r.best.edges, r.best.verts] == e["best"] and sha(r.witness) == e["witness"]
+        assert [[t.iter, t.rho.edges, t.rho.verts, t.n, t.m, t.width] for t in r.trace.iters] == e["trace"]
+        assert sha(r.trace.final_vertices) == e["final_vertices"] and r.max_width == e["max_width"]
+
+
+def test_medium_rmat_vs_oracle(dg, orc):
+    """RMAT-17 (beyond the fixtures): every output of a T=10 run and the
+    per-iteration Greedy++ state against the oracle."""
+    u, v = dg.gen_rmat(17, 16 << 17, 17)
+    h = orc.build(u, v)
+    g = dg.Graph.from_pairs(u, v)
+    assert same_csr(g, h)
+    d = dg.exact_coreness(g)
+    lab, kmax, rounds = orc.coreness(h)
+    assert np.array_equal(d.labels, lab) and (d.kmax, d.peel_rounds) == (kmax, rounds)
+    a = dg.approx_coreness(g, 3, 2)
+    al, ak, ar = orc.coreness(h, True, 3, 2)
+    assert np.array_equal(a.labels, al) and (a.kmax, a.peel_rounds) == (ak, ar)
+    core = dg.get_core(g, d, (kmax + 1) // 2)
+    hc, _ = orc.get_core(h, lab, (kmax + 1) // 2)
+    assert same_csr(core, hc)
+    ld, lh = np.zeros(core.n, np.uint64), np.zeros(core.n, np.uint64)
+    for _ in range(6):
+        p = dg.load_peel_order(core, ld).perm
+        assert np.array_equal(p, orc.peel_order(hc, lh))
+        dg.density_and_load_update(core, p, ld)
+        _, lh, _, _ = orc.density_update(hc, p, lh)
+        assert np.array_equal(ld, lh)
+    for pr in ("exact", "approx", "hybrid"):
+        for alg in ("peel", "sort"):
+            r = dg.run(g, dg.RunConfig(algorithm=alg, pruning=pr, iterations=10))
+            o = orc.run(h, ORunConfig(algorithm=alg, pruning=pr, iterations=10))
+            assert (r.best.edges, r.best.verts) == o.best and np.array_equal(r.witness, o.witness)
+            assert [(t.iter, t.rho.edges, t.rho.verts, t.n, t.m, t.width)
+                    for t in r.trace.iters] == o.trace
+            assert np.array_equal(r.trace.final_vertices, o.final_vertices)
+
+
+def test_cpp_dropin_api_on_device():
+    """The reference's pinned unit-test behaviour through include/densegraph/*.hpp."""
+    lib = os.path.join(ROOT, "paper_2311_04333_b200")
+    out = os.path.join("/tmp", "dg_test_api.bin")
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "test_api.cpp"), "-o", out, "-L", lib, "-ldg_b200",
+           f"-Wl,-rpath,{lib}"]
+    subprocess.run(cmd, check=True)
+    r = subprocess.run([out], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
