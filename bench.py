@@ -1,0 +1,389 @@
+#!/usr/bin/env python3
+"""bench.py -- Greedy++ edges/s per iteration and k-core edges/s on B200.
+
+Workload (BASELINE.json configs[1], the metric's N=1 config): RMAT scale 22,
+edge factor 16 (67,108,864 seeded samples, a=.57 b=.19 c=.19 d=.05),
+symmetrised / deduplicated / loop-free u32 CSR; exact k-core -> ceil(kmax/2)-core
+-> Greedy++ T=20 (eps=0.05 is advisory: explicit T wins, framework.cpp:99-104)
+with adaptive re-pruning -> witness.  One STEP = that whole hot path on the
+resident CSR.  Inputs are synthetic (seeded generators; no dataset).
+
+  value   Greedy++ edges/s per iteration = sum_it m_cur / sum_it t_iter over the
+          timed steps, t_iter = CUDA-event time of ordering + Alg. 3
+  kcore   k-core edges/s = m / t(k-core kernel), CUDA events
+  e2e     the same numerator through the C ABI from pinned HOST buffers:
+          H2D of the CSR + k-core + prune + T iterations + D2H of the results,
+          wall-clocked -- every overhead is charged to the iterations
+  roofline  dominant kernel (the Greedy++ batch-peel kernel) against the
+          measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the unmodified reference library (oracle/_ref) on this host
+
+--impl reference runs only the reference library (rank 0), same metric.
+Multi-GPU (torchrun): every rank runs the full step on its own GPU
+("replicas", weak scaling), timing = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+METRIC = "Greedy++ edges/sec per iteration and k-core edges/sec; % of HBM roofline"
+CONFIGS = {
+    # BASELINE.json configs[1]
+    "rmat22": dict(kind="rmat", scale=22, edge_factor=16, seed=22, T=20, eps=0.05),
+    # configs[0] (ER n=100k m=1M + planted 300-block p=0.5), T=10
+    "er_planted": dict(kind="er", n=100000, m=1000000, block=300, seed=1, T=10, eps=0.1),
+    # configs[3]: RMAT-26, T=10
+    "rmat26": dict(kind="rmat", scale=26, edge_factor=16, seed=26, T=10, eps=0.1),
+    # configs[2]: Chung-Lu n=50M, 500M endpoint pairs, exponent 2.1, T=20
+    "chunglu50m": dict(kind="cl", n=50_000_000, pairs=500_000_000, seed=50, T=20, eps=0.05),
+    # small config for quick checks / profiling
+    "rmat18": dict(kind="rmat", scale=18, edge_factor=16, seed=18, T=20, eps=0.05),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.samples, self.proc, self.t = [], None, None
+        self.window = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append((time.time(), parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        inwin = [p for (t, p) in self.samples if t0 - 0.15 <= t <= t1 + 0.15] or \
+                [p for (_, p) in self.samples]
+        if not inwin:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = sorted(float(p[0]) for p in inwin if p[0].replace(".", "").isdigit())
+        mx = max((float(p[1]) for p in inwin if p[1].replace(".", "").isdigit()), default=None)
+        reasons = sorted({names[i] for p in inwin for i in range(4) if p[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(inwin)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
+def allreduce(vals, op, world, local):
+    if world == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+# ------------------------------------------------------------------ inputs
+def host_pairs(cfg):
+    """Seeded pairs on the host (oracle generators; used by the reference arm)."""
+    from oracle import Oracle
+    orc = Oracle()
+    if cfg["kind"] == "rmat":
+        return orc.gen_rmat(cfg["scale"], cfg["edge_factor"] << cfg["scale"], cfg["seed"])
+    if cfg["kind"] == "er":
+        return orc.gen_er_planted(cfg["n"], cfg["m"], cfg["block"], cfg["seed"])
+    return orc.gen_chung_lu(cfg["n"], cfg["pairs"], cfg["seed"])
+
+
+def device_graph(dg, cfg):
+    """Generate the seeded pairs on the device and build the CSR there."""
+    if cfg["kind"] == "er":
+        u, v = host_pairs(cfg)
+        return dg.Graph.from_pairs(u, v)
+    import ctypes as C
+    k = cfg["edge_factor"] << cfg["scale"] if cfg["kind"] == "rmat" else cfg["pairs"]
+    bu, bv = dg.DeviceBuffer(8 * k), dg.DeviceBuffer(8 * k)
+    if cfg["kind"] == "rmat":
+        dg._chk(dg.LIB.dg_gen_rmat(cfg["scale"], k, cfg["seed"], C.c_void_p(bu.ptr),
+                                   C.c_void_p(bv.ptr), 1))
+    else:
+        R = float(cfg["n"]) ** (1.0 / 11.0)
+        dg._chk(dg.LIB.dg_gen_chung_lu(cfg["n"], k, R, cfg["seed"], C.c_void_p(bu.ptr),
+                                       C.c_void_p(bv.ptr), 1))
+    g = dg.Graph.from_device_pairs(bu.ptr, bv.ptr, k)
+    bu.free()
+    bv.free()
+    return g
+
+
+def pinned_copy(a):
+    import numpy as np
+    import torch
+    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    out = t.numpy().view(a.dtype)
+    np.copyto(out, a)
+    return out, t
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import Oracle, Reference, RunConfig, reference_available
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "metric": METRIC,
+                          "unavailable": "oracle/_ref/libdgref.so was not built (needs /root/reference at build time)"}))
+        return 0
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    u, v = host_pairs(cfg)
+    h = Oracle().build(u, v)
+    del u, v
+    rg = ref.from_csr(h)
+    rcfg = RunConfig(iterations=cfg["T"], epsilon=cfg["eps"])
+    for _ in range(args.warmup):
+        ref.run(rg, rcfg, threads=threads)
+    edges = ms_it = 0.0
+    t_steps = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = ref.run(rg, rcfg, threads=threads)
+        t_steps.append((time.perf_counter() - t0) * 1e3)
+        edges += sum(t[4] for t in r.trace)
+        ms_it += sum(r.iter_ms)
+    value = edges / (ms_it / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sum(t_steps) / len(t_steps), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": workload_config(args.config, cfg, h.n, h.m, world),
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} full reference run()s (k-core + prune + T={cfg['T']} Greedy++) of the same graph; value = sum m_cur / sum IterRecord.ms"},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_detail": {"init_ms": r.times[1], "coreness_ms_incl_get_core": r.times[0],
+                             "total_ms": r.times[2], "iter_ms": r.iter_ms[:len(r.trace)]},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(name, cfg, n, m, world):
+    c = {"workload": f"{name}: exact k-core prune + Greedy++ T={cfg['T']} (eps={cfg['eps']} advisory)",
+         "n": int(n), "m": int(m), "T": cfg["T"], "epsilon": cfg["eps"], "seed": cfg["seed"],
+         "l2": "flushed between steps (256 MiB memset); CSR also exceeds L2",
+         "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"}
+    if cfg["kind"] == "rmat":
+        c.update(generator="RMAT a=.57 b=.19 c=.19 d=.05", scale=cfg["scale"],
+                 samples=cfg["edge_factor"] << cfg["scale"])
+    elif cfg["kind"] == "er":
+        c.update(generator="ER + planted block p=0.5", block=cfg["block"])
+    else:
+        c.update(generator="Chung-Lu power law exponent 2.1", pairs=cfg["pairs"])
+    return c
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, cfg, rank, world, local):
+    import numpy as np
+    import paper_2311_04333_b200 as dg
+    dg.set_device(local)
+    hbm, peak_kind = peaks()
+    g = device_graph(dg, cfg)
+    n, m = g.n, g.m
+    rcfg = dg.RunConfig(iterations=cfg["T"], epsilon=cfg["eps"])
+    for _ in range(args.warmup):
+        dg.run(g, rcfg)
+    clocks = Clocks(local)
+    time.sleep(0.25)
+    res = []
+    launches0 = dg.launch_count()
+    barrier(world)
+    dg.synchronize()
+    t_start = time.time()
+    for _ in range(args.steps):
+        dg.flush_l2()
+        res.append(dg.run(g, rcfg))
+    dg.synchronize()
+    barrier(world)
+    t_end = time.time()
+    launches = dg.launch_count() - launches0
+    clk = clocks.summary(t_start, t_end)
+    clocks.stop()
+
+    edges = sum(it.m for r in res for it in r.trace.iters)
+    it_ms = sum(it.ms for r in res for it in r.trace.iters)
+    order_ms = sum(it.order_ms for r in res for it in r.trace.iters)
+    batches = sum(it.batches for r in res for it in r.trace.iters)
+    peel_bytes = sum(8 * (it.n + 1) + 8 * it.m + 16 * it.n for r in res for it in r.trace.iters)
+    kc_ms = sum(r.trace.init.coreness_kernel_ms for r in res)
+    dev_ms = sum(r.device_ms for r in res)
+    # max over ranks for times, sum for work
+    it_ms_max, kc_ms_max, dev_ms_max, order_ms_max = allreduce([it_ms, kc_ms, dev_ms, order_ms],
+                                                               "max", world, local)
+    edges_all, kc_edges_all = allreduce([float(edges), float(m * args.steps)], "sum", world, local)
+    value = edges_all / (it_ms_max / 1e3)
+    kcore_value = kc_edges_all / (kc_ms_max / 1e3)
+    peel_achieved = peel_bytes / (order_ms / 1e3) / 1e9
+    kc_bytes = 8 * m + 16 * n + 8
+    kc_achieved = kc_bytes * args.steps / (kc_ms / 1e3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": workload_config(args.config, cfg, n, m, world),
+        "kcore": {"value": kcore_value, "unit": "edges/s",
+                  "ms": kc_ms / args.steps, "peel_rounds": res[0].trace.init.peel_rounds,
+                  "kmax": res[0].trace.init.kmax,
+                  "roofline": {"bound": "hbm", "achieved": kc_achieved, "peak": hbm,
+                               "unit": "GB/s", "frac": kc_achieved / hbm,
+                               "algorithmic_bytes": kc_bytes, "peak_kind": peak_kind}},
+        "roofline": {"bound": "hbm", "achieved": peel_achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": peel_achieved / hbm, "traffic": None,
+                     "kernel": "k_peel (Greedy++ batch peel, fused Alg.3 charges)",
+                     "bytes_per_launch": "8(n+1) offs + 8m adj + 8n loads + 4n perm + 4n charges",
+                     "peak_kind": peak_kind},
+        "greedy": {"iterations": sum(len(r.trace.iters) for r in res),
+                   "batches_per_iter": batches / max(1, sum(len(r.trace.iters) for r in res)),
+                   "us_per_batch": order_ms * 1e3 / max(1, batches),
+                   "order_ms_per_iter": order_ms / max(1, sum(len(r.trace.iters) for r in res)),
+                   "update_ms_per_iter": (it_ms - order_ms) / max(1, sum(len(r.trace.iters) for r in res)),
+                   "core_n_m": [res[0].trace.init.pruned_n, res[0].trace.init.pruned_m],
+                   "reprunes": res[0].reprunes,
+                   "best": [res[0].best.edges, res[0].best.verts],
+                   "witness_size": len(res[0].witness)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+
+    # ---- e2e through the C ABI from pinned host buffers
+    offs, adj, orig = g.download()
+    p_offs, _t1 = pinned_copy(offs)
+    p_adj, _t2 = pinned_copy(adj)
+    p_orig, _t3 = pinned_copy(orig)
+    e2e_edges = e2e_s = 0.0
+    d2h = 0
+    for _ in range(max(1, min(args.steps, 5))):
+        dg.flush_l2()
+        t0 = time.perf_counter()
+        g2 = dg.Graph.from_csr(p_offs, p_adj, p_orig)
+        r = dg.run(g2, rcfg)
+        del g2
+        e2e_s += time.perf_counter() - t0
+        e2e_edges += sum(it.m for it in r.trace.iters)
+        d2h = 8 * (len(r.witness) + len(r.trace.final_vertices)) + 80 * len(r.trace.iters) + 64
+    e2e_s = allreduce([e2e_s], "max", world, local)[0]
+    e2e_edges = allreduce([e2e_edges], "sum", world, local)[0]
+    line["e2e"] = {"value": e2e_edges / e2e_s, "unit": "edges/s",
+                   "h2d_bytes_per_step": int(p_offs.nbytes + p_adj.nbytes + p_orig.nbytes),
+                   "d2h_bytes_per_step": int(d2h),
+                   "includes": "H2D CSR + k-core + prune + T iterations + witness recount + D2H"}
+
+    # ---- CPU baseline: the reference library on this host (rank 0, N=1)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, offs, adj, orig)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(cfg, offs, adj, orig):
+    from oracle import HostGraph, Reference, RunConfig, reference_available
+    if not reference_available():
+        return {"value": None, "unit": "edges/s", "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    rg = ref.from_csr(HostGraph(offs, adj, orig))
+    n, m, _ = rg.info()
+    t0 = time.perf_counter()
+    ref.coreness(rg)
+    kc_s = time.perf_counter() - t0
+    r = ref.run(rg, RunConfig(iterations=cfg["T"], epsilon=cfg["eps"]), threads=threads)
+    edges = sum(t[4] for t in r.trace)
+    return {"value": edges / (sum(r.iter_ms) / 1e3), "unit": "edges/s", "cores": threads,
+            "kind": "reference",
+            "sample": f"one full reference run() (T={cfg['T']}) + one exact_coreness on the same graph",
+            "kcore_value": m / kc_s, "run_total_ms": r.times[2], "init_ms": r.times[1]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="rmat22", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank, world, local = dist_init()
+    if args.impl == "reference":
+        rc = run_reference(args, cfg, rank, world)
+    else:
+        rc = run_ours(args, cfg, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -165,6 +165,7 @@ typedef struct { /* RunResult + RunTrace/InitRecord (framework.hpp:35-60) */
   double coreness_kernel_ms; /* the k-core kernel alone */
   double init_ms, total_ms;
   double reprune_ms;     /* all mid-run re-prune compactions */
+  double device_ms;      /* CUDA-event span of the whole run on the library stream */
 } dg_run_result;
 
 /* run(g, cfg) (framework.hpp:68, framework.cpp:46-180): Algorithm 1 on the
@@ -190,6 +191,23 @@ dg_status dg_device_alloc(uint64_t bytes, void** ptr);
 dg_status dg_device_free(void* ptr);
 dg_status dg_memcpy(void* dst, const void* src, uint64_t bytes, int kind /* 1 h2d, 2 d2h, 3 d2d */);
 dg_status dg_synchronize(void);
+
+/* Select the CUDA device for this thread's subsequent calls (one process per GPU). */
+dg_status dg_set_device(int device);
+/* Number of this library's own kernels launched so far in this process. */
+uint64_t dg_launch_count(void);
+/* Evict L2 by writing a 256 MiB scratch buffer (bench hygiene between steps). */
+dg_status dg_flush_l2(void);
+
+/* Diagnostic latency floors (ns per op): 0 grid barrier (this library's),
+ * 1 cooperative-groups grid.sync, 2 cluster barrier (8 CTAs), 3 CTA barrier
+ * (1024 threads), 4 dependent L2 load, 5 shared atomicAdd per warp
+ * instruction (spread addresses), 6 plain shared load+store per warp instr. */
+dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op);
+/* Diagnostic: thread-0 SM cycles of the last Greedy++ peel launch spent in
+ * S1 (min scan), S2 (batch extraction), S3 (removal), its batch count, S3
+ * cycles of single-vertex batches, their count, #batches > 32, n. */
+dg_status dg_peel_profile(uint64_t out[16]);
 
 #ifdef __cplusplus
 }

@@ -482,6 +482,24 @@ class RunResult:
     trace: RunTrace
     reprunes: int = 0
     reprune_ms: float = 0.0
+    device_ms: float = 0.0
+
+
+def set_device(device: int) -> None:
+    _chk(LIB.dg_set_device(device))
+
+
+def launch_count() -> int:
+    """Kernels of this library launched so far in this process."""
+    return LIB.dg_launch_count()
+
+
+def flush_l2() -> None:
+    _chk(LIB.dg_flush_l2())
+
+
+def synchronize() -> None:
+    _chk(LIB.dg_synchronize())
 
 
 def run(g: Graph, cfg: Optional[RunConfig] = None) -> RunResult:
@@ -503,7 +521,7 @@ def run(g: Graph, cfg: Optional[RunConfig] = None) -> RunResult:
     tr = RunTrace(init, iters, res.slack_violations, fin[: res.final_n].copy())
     return RunResult(Density(res.best_edges, res.best_verts), wit[: res.witness_size].copy(),
                      res.witness_edges, res.iterations, res.max_width, res.total_ms, tr,
-                     res.reprunes, res.reprune_ms)
+                     res.reprunes, res.reprune_ms, res.device_ms)
 
 
 # ------------------------------------------------------------------ synthetic inputs

@@ -42,7 +42,8 @@ class DgRunResult(C.Structure):
                 ("pruned_n", C.c_uint64), ("pruned_m", C.c_uint64), ("final_n", C.c_uint64),
                 ("peel_rounds", C.c_uint32), ("reprunes", C.c_uint32),
                 ("coreness_ms", C.c_double), ("coreness_kernel_ms", C.c_double),
-                ("init_ms", C.c_double), ("total_ms", C.c_double), ("reprune_ms", C.c_double)]
+                ("init_ms", C.c_double), ("total_ms", C.c_double), ("reprune_ms", C.c_double),
+                ("device_ms", C.c_double)]
 
 
 GP = C.c_void_p  # dg_graph*
@@ -80,6 +81,11 @@ PROTOTYPES = {
     "dg_device_free": (C.c_int, [C.c_void_p]),
     "dg_memcpy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int]),
     "dg_synchronize": (C.c_int, []),
+    "dg_set_device": (C.c_int, [C.c_int]),
+    "dg_launch_count": (C.c_uint64, []),
+    "dg_flush_l2": (C.c_int, []),
+    "dg_microbench": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_double)]),
+    "dg_peel_profile": (C.c_int, [u64p]),
 }
 
 

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <atomic>
 #include <mutex>
 #include <numeric>
 #include <vector>
@@ -59,6 +60,11 @@ int num_sms() {
 }
 
 void stream_sync() { DG_CUDA(cudaStreamSynchronize(stream())); }
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 
@@ -166,6 +172,8 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
     throw DgError(DG_E_PARAM, "unknown algorithm or pruning mode");
   *res = dg_run_result{};
   const double t0 = now_ms();
+  Events span;
+  DG_CUDA(cudaEventRecord(span.e[0], stream()));
   GraphPtr owned;
   const dg_graph* cur = g;
   DevBuf<uint32_t> labels;
@@ -224,7 +232,8 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
 
   DevBuf<uint64_t> loads(cur->n), wit(cur->n);
   loads.zero();
-  DevBuf<uint32_t> perm(cur->n), charges(cur->n);
+  DevBuf<uint32_t> perm(cur->n), charges;  // charges: sort path only
+  DevBuf<uint64_t> raw(cur->n);             // fused peel charges
   DevBuf<Alg3Out> dout(1);
   DevBuf<unsigned long long> dbat(1);
   KeyRange kr{0, cur->maxdeg};
@@ -235,14 +244,17 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
     const uint64_t n = cur->n;
     DG_CUDA(cudaEventRecord(ev.e[0], stream()));
     if (cfg->algorithm == 0) {
-      peel_order(*cur, loads.get(), kr, false, perm.get(), charges.get(), dbat.get());
+      peel_order(*cur, loads.get(), kr, false, perm.get(), raw.get(), dbat.get());
     } else {
       sort_order(n, loads.get(), perm.get());
+      if (charges.n != n) charges.alloc(n);
       charges_from_perm(*cur, perm.get(), charges.get());
     }
     DG_CUDA(cudaEventRecord(ev.e[1], stream()));
     const uint64_t allowed = cfg->algorithm == 0 ? delta_cur : 0;
-    alg3(*cur, perm.get(), charges.get(), loads.get(), cfg->slack_samples, allowed,
+    alg3(*cur, perm.get(), cfg->algorithm == 0 ? nullptr : charges.get(),
+         cfg->algorithm == 0 ? raw.get() : nullptr, kr.min_load, loads.get(), cfg->slack_samples,
+         allowed,
          0x5eed0000ULL + it, nullptr, dout.get());
     DG_CUDA(cudaEventRecord(ev.e[2], stream()));
     Alg3Out o;
@@ -298,7 +310,7 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
         owned = std::move(next);
         cur = owned.get();
         perm.alloc(cur->n);
-        charges.alloc(cur->n);
+        raw.alloc(cur->n);
         delta_cur = cur->maxdeg;
         thresh = nt;
         kr = key_range(*cur, loads.get());
@@ -339,7 +351,9 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
   if (witness) d2h(witness, wit.get(), std::min(nwit, witness_cap));
   res->final_n = cur->n;
   if (final_ids) d2h(final_ids, cur->orig.get(), std::min<uint64_t>(cur->n, final_cap));
+  DG_CUDA(cudaEventRecord(span.e[1], stream()));
   stream_sync();
+  res->device_ms = span.ms(0, 1);
   res->total_ms = now_ms() - t0;
 }
 
@@ -518,10 +532,11 @@ dg_status dg_peel_order(const dg_graph* g, const uint64_t* loads, int one_at_a_t
   if (!g) throw DgError(DG_E_PARAM, "null graph");
   if (g->n == 0) return DG_OK;
   DevBuf<uint64_t> dl = stage(loads, g->n, 0);
-  DevBuf<uint32_t> dp(g->n), dc(g->n);
+  DevBuf<uint32_t> dp(g->n);
+  DevBuf<uint64_t> dr(g->n);
   DevBuf<unsigned long long> nb(1);
   KeyRange kr = key_range(*g, dl.get());
-  peel_order(*g, dl.get(), kr, one_at_a_time != 0, dp.get(), dc.get(), nb.get());
+  peel_order(*g, dl.get(), kr, one_at_a_time != 0, dp.get(), dr.get(), nb.get());
   d2h(perm, dp.get(), g->n);
   stream_sync();
   DG_API_END
@@ -547,7 +562,8 @@ dg_status dg_density_load_update(const dg_graph* g, const uint32_t* perm, uint64
   DevBuf<uint64_t> dl = stage(loads, n, 0), ds(suffix_edges ? n : 0);
   DevBuf<Alg3Out> o(1);
   charges_from_perm(*g, dp.get(), dc.get());
-  alg3(*g, dp.get(), dc.get(), dl.get(), 0, 0, 0, suffix_edges ? ds.get() : nullptr, o.get());
+  alg3(*g, dp.get(), dc.get(), nullptr, 0, dl.get(), 0, 0, 0, suffix_edges ? ds.get() : nullptr,
+       o.get());
   Alg3Out h;
   d2h(&h, o.get(), 1);
   d2h(loads, dl.get(), n);
@@ -569,11 +585,12 @@ dg_status dg_charikar_peel(const dg_graph* g, dg_outcome* out) {
   if (n == 0) return DG_OK;
   DevBuf<uint64_t> dl(n);
   dl.zero();
-  DevBuf<uint32_t> dp(n), dc(n);
+  DevBuf<uint32_t> dp(n);
+  DevBuf<uint64_t> dr(n);
   DevBuf<unsigned long long> nb(1);
   DevBuf<Alg3Out> o(1);
-  peel_order(*g, dl.get(), KeyRange{0, g->maxdeg}, false, dp.get(), dc.get(), nb.get());
-  alg3(*g, dp.get(), dc.get(), dl.get(), 0, 0, 0, nullptr, o.get());
+  peel_order(*g, dl.get(), KeyRange{0, g->maxdeg}, false, dp.get(), dr.get(), nb.get());
+  alg3(*g, dp.get(), nullptr, dr.get(), 0, dl.get(), 0, 0, 0, nullptr, o.get());
   Alg3Out h;
   d2h(&h, o.get(), 1);
   stream_sync();
@@ -601,7 +618,8 @@ dg_status dg_slack_violations(uint64_t n, const uint32_t* perm, const uint64_t* 
   dc.zero();
   DevBuf<uint64_t> dl = stage(loads, n, 0);
   DevBuf<Alg3Out> o(1);
-  alg3(g0, dp.get(), dc.get(), dl.get(), samples, allowed_slack, seed, nullptr, o.get());
+  alg3(g0, dp.get(), dc.get(), nullptr, 0, dl.get(), samples, allowed_slack, seed, nullptr,
+       o.get());
   Alg3Out h;
   d2h(&h, o.get(), 1);
   stream_sync();
@@ -684,6 +702,26 @@ dg_status dg_memcpy(void* dst, const void* src, uint64_t bytes, int kind) {
 
 dg_status dg_synchronize(void) {
   DG_API_BEGIN
+  stream_sync();
+  DG_API_END
+}
+
+dg_status dg_set_device(int device) {
+  DG_API_BEGIN
+  DG_CUDA(cudaSetDevice(device));
+  stream();
+  DG_API_END
+}
+
+uint64_t dg_launch_count(void) { return g_launches.load(); }
+
+dg_status dg_flush_l2(void) {
+  DG_API_BEGIN
+  static thread_local void* scratch[kMaxDev] = {};
+  const int d = cur_dev();
+  const size_t bytes = size_t(256) << 20;
+  if (!scratch[d]) DG_CUDA(cudaMalloc(&scratch[d], bytes));
+  DG_CUDA(cudaMemsetAsync(scratch[d], d + 1, bytes, stream()));
   stream_sync();
   DG_API_END
 }

@@ -37,7 +37,12 @@ struct DgError : std::runtime_error {
     if (e_ != cudaSuccess) ::dgb::throw_cuda(e_, #call, __FILE__, __LINE__); \
   } while (0)
 
-#define DG_CHECK_LAUNCH() DG_CUDA(cudaGetLastError())
+void count_launch();
+#define DG_CHECK_LAUNCH()            \
+  do {                               \
+    DG_CUDA(cudaGetLastError());     \
+    ::dgb::count_launch();           \
+  } while (0)
 
 // The library's stream on the current device (one per device, created
 // lazily).  Every entry point enqueues on it and synchronises before
@@ -68,7 +73,10 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) DG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream()));
+    // +16 bytes of slack: kernels may read a whole 16-byte vector that
+    // straddles the end of an array (e.g. the last adjacency quad)
+    if (count)
+      DG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T) + 16, stream()));
   }
   void release() {
     if (p) cudaFreeAsync(p, stream());
@@ -213,30 +221,54 @@ struct GridBarrier {
   uint32_t pad;
 };
 
-__device__ __forceinline__ bool grid_sync(GridBarrier* b, uint32_t nblocks) {
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Only thread 0 of each CTA touches the barrier words; after the barrier it
+// runs `fetch()` (e.g. loads the phase's global scalars into shared memory)
+// so the rest of the CTA never hammers one L2 line.  *s_abort is a shared
+// word the CTA reads after the closing __syncthreads.
+template <class Fetch>
+__device__ __forceinline__ bool grid_sync(GridBarrier* b, uint32_t nblocks, uint32_t* s_abort,
+                                          Fetch fetch) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    uint32_t g = ld_acquire_u32(&b->gen);
+    // One arrival word whose top bit flips when the last CTA arrives: CTA 0
+    // adds 2^31 - (nblocks - 1), every other CTA adds 1, so the sum of one
+    // barrier episode is exactly 2^31.  Waiters poll the same word; no reset
+    // store, one atomic round trip on the critical path.
+    const uint32_t add = blockIdx.x == 0 ? 0x80000000u - (nblocks - 1) : 1u;
     __threadfence();
-    uint32_t arrived = atomicAdd(&b->count, 1u);
-    if (arrived == nblocks - 1) {
-      __threadfence();
-      b->count = 0;
-      st_release_u32(&b->gen, g + 1);
-    } else {
-      long long t0 = clock64();
-      while (ld_acquire_u32(&b->gen) == g) {
-        if (ld_acquire_u32(&b->abort)) break;
-        if (clock64() - t0 > (1LL << 33)) {  // ~4 s at 2 GHz
+    const uint32_t old = atomicAdd(&b->count, add);
+    const long long t0 = clock64();
+    uint32_t spins = 0;
+    while (((old ^ ld_acquire_u32(&b->count)) & 0x80000000u) == 0) {
+      if ((++spins & 1023u) == 0) {
+        if (ld_relaxed_u32(&b->abort)) break;
+        if (clock64() - t0 > (1LL << 33)) {  // ~4 s at 2 GHz: give up, do not hang
           atomicExch(&b->abort, 1u);
           break;
         }
       }
-      __threadfence();
     }
+    __threadfence();
+    *s_abort = ld_relaxed_u32(&b->abort);
+    fetch();
   }
   __syncthreads();
-  return *(volatile uint32_t*)&b->abort == 0;
+  return *s_abort == 0;
+}
+
+__device__ __forceinline__ bool grid_sync(GridBarrier* b, uint32_t nblocks, uint32_t* s_abort) {
+  return grid_sync(b, nblocks, s_abort, [] {});
 }
 
 }  // namespace dgb

@@ -45,12 +45,15 @@ struct KeyRange {
   uint64_t max_key = 0;   // max over v of load(v) - base + deg(v)
 };
 // Greedy++ ordering (refine.cpp:20-156) with Alg. 3 charges fused:
-// d_charges[i] = A[i] of density_and_load_update for position i.
+// d_raw[i] = key at removal - #same-batch smaller neighbours, so that
+// A[i] = d_raw[i] - (load(perm[i]) - kr.min_load)  (see peel_kernel.cuh).
 // *d_batches (device) receives the number of batches.
 void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
-                bool one_at_a_time, uint32_t* d_perm, uint32_t* d_charges,
+                bool one_at_a_time, uint32_t* d_perm, uint64_t* d_raw,
                 unsigned long long* d_batches);
 KeyRange key_range(const dg_graph& g, const uint64_t* d_loads);
+// thread-0 cycle split (S1, S2, S3, batches) of the last peel launch
+void peel_profile(unsigned long long out[16]);
 void sort_order(uint64_t n, const uint64_t* d_loads, uint32_t* d_perm);
 // A[i] from an arbitrary permutation (refine.cpp:186-199); throws InvariantError
 // on a non-permutation.
@@ -64,7 +67,9 @@ struct Alg3Out {  // device-written scalars of one update
 };
 // Suffix sums, exact first-strict argmax, width, loads += A, slack audit,
 // next KeyRange; result in *d_out (device).  d_suffix optional.
+// Charges come either final (d_charges) or raw from the fused peel (d_raw, base).
 void alg3(const dg_graph& g, const uint32_t* d_perm, const uint32_t* d_charges,
+          const uint64_t* d_raw, uint64_t raw_base,
           uint64_t* d_loads, uint64_t slack_samples, uint64_t slack_allowed, uint64_t slack_seed,
           uint64_t* d_suffix, Alg3Out* d_out);
 

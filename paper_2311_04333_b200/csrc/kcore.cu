@@ -74,7 +74,18 @@ struct Smem {
   uint32_t cnt;
   unsigned long long baseF, baseL;
   uint32_t minv;
+  // phase scalars fetched by thread 0 after each grid barrier
+  uint32_t abort;
+  unsigned long long b_front, b_live;
+  uint32_t b_minv, b_ovf;
 };
+
+__device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
+  s.b_front = ld_relaxed_u64(&acc->front);
+  s.b_live = ld_relaxed_u64(&acc->live);
+  s.b_minv = ld_relaxed_u32(&acc->minv);
+  s.b_ovf = ld_relaxed_u32(&acc->ovf);
+}
 
 __device__ __forceinline__ uint32_t deg_full(const uint64_t* offs, uint32_t v) {
   return uint32_t(offs[v + 1] - offs[v]);
@@ -194,8 +205,8 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
         x = warp_min(x);
         if (threadIdx.x == 0 && x != kUnset) atomicMin(&acc->minv, x);
       }
-      if (!grid_sync(a.bar, nb)) break;
-      const uint64_t gmin = *(volatile uint32_t*)&acc->minv;
+      if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
+      const uint64_t gmin = s.b_minv;
       if (gmin == kUnset) {  // remaining > 0 but nothing alive: inconsistent
         if (blockIdx.x == 0 && threadIdx.x == 0) a.out[2] = 2;
         break;
@@ -217,11 +228,11 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       uint32_t* cse = (f & 1) ? a.cse1 : a.cse0;
       collect(a, livec, implicit, live_in, lv ? a.live0 : a.live1, uint32_t(bound),
               uint32_t(label), fr, fa, cse, acc, s);
-      if (!grid_sync(a.bar, nb)) break;
-      const unsigned long long pk = *(volatile unsigned long long*)&acc->front;
+      if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
+      const unsigned long long pk = s.b_front;
       Fc = uint32_t(pk >> 36);
       Ftot = pk & M36;
-      livec = uint32_t(*(volatile unsigned long long*)&acc->live);
+      livec = uint32_t(s.b_live);
       lv ^= 1;
       implicit = false;
       if (Fc == 0) {
@@ -303,27 +314,27 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
                         nacc, s);
       }
     }
-    if (!grid_sync(a.bar, nb)) break;
+    if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, nacc); })) break;
     ++f;
-    if (*(volatile uint32_t*)&nacc->ovf) {
+    if (s.b_ovf) {
       uint32_t* fr = (f & 1) ? a.fr1 : a.fr0;
       uint64_t* fa = (f & 1) ? a.fa1 : a.fa0;
       uint32_t* cse = (f & 1) ? a.cse1 : a.cse0;
       collect(a, livec, implicit, lv ? a.live1 : a.live0, lv ? a.live0 : a.live1, uint32_t(bound),
               uint32_t(label), fr, fa, cse, nacc, s);
-      if (!grid_sync(a.bar, nb)) break;
-      livec = uint32_t(*(volatile unsigned long long*)&nacc->live);
+      if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, nacc); })) break;
+      livec = uint32_t(s.b_live);
       lv ^= 1;
       implicit = false;
     }
-    const unsigned long long pk = *(volatile unsigned long long*)&nacc->front;
+    const unsigned long long pk = s.b_front;
     Fc = uint32_t(pk >> 36);
     Ftot = pk & M36;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.out[0] = kmax;
     a.out[1] = rounds;
-    if (*(volatile uint32_t*)&a.bar->abort) a.out[2] = 4;
+    if (ld_relaxed_u32(&a.bar->abort)) a.out[2] = 4;
   }
 }
 

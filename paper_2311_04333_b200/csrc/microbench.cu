@@ -1,0 +1,131 @@
+// microbench.cu -- latency floors that bound the per-round (k-core) and
+// per-batch (Greedy++) costs on this B200: grid barrier, cooperative-groups
+// grid.sync, cluster barrier, CTA barrier, dependent L2 load chain, shared
+// atomics (spread / plain RMW).  Diagnostic only (dg_microbench).
+#include <cooperative_groups.h>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dgb {
+namespace {
+
+__global__ void k_mb_grid(GridBarrier* b, uint64_t iters) {
+  __shared__ uint32_t ab;
+  for (uint64_t i = 0; i < iters; ++i)
+    if (!grid_sync(b, gridDim.x, &ab)) break;
+}
+
+__global__ void k_mb_cg(uint64_t iters) {
+  cg::grid_group g = cg::this_grid();
+  for (uint64_t i = 0; i < iters; ++i) g.sync();
+}
+
+__global__ void __cluster_dims__(8, 1, 1) k_mb_cluster(uint64_t iters) {
+  cg::cluster_group c = cg::this_cluster();
+  for (uint64_t i = 0; i < iters; ++i) c.sync();
+}
+
+__global__ void k_mb_bar(uint64_t iters, uint32_t* sink) {
+  uint32_t x = threadIdx.x;
+  for (uint64_t i = 0; i < iters; ++i) {
+    __syncthreads();
+    x = x * 1664525u + 1013904223u;
+  }
+  if (x == 7) *sink = x;
+}
+
+__global__ void k_mb_chase(const uint32_t* next, uint64_t iters, uint32_t* sink) {
+  uint32_t p = 0;
+  for (uint64_t i = 0; i < iters; ++i) p = next[p];
+  *sink = p;
+}
+
+__global__ void k_mb_atoms(uint64_t iters, uint32_t* sink, int plain) {
+  __shared__ uint32_t a[8192];
+  for (uint32_t i = threadIdx.x; i < 8192; i += blockDim.x) a[i] = 0;
+  __syncthreads();
+  uint32_t idx = (threadIdx.x * 2654435761u) & 8191u;
+  for (uint64_t i = 0; i < iters; ++i) {
+    if (plain)
+      a[idx] = a[idx] + 1;
+    else
+      atomicAdd(&a[idx], 1u);
+    idx = (idx + 1031u) & 8191u;
+  }
+  __syncthreads();
+  if (a[threadIdx.x] == 0xdeadbeef) *sink = 1;
+}
+
+__global__ void k_mb_init_chase(uint32_t* next, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    next[i] = uint32_t((uint64_t(i) * 40503u + 7919u) % n);  // full-cycle-ish stride walk
+}
+
+}  // namespace
+}  // namespace dgb
+
+using namespace dgb;
+
+extern "C" dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op) {
+  try {
+    DevBuf<uint32_t> sink(1);
+    cudaEvent_t e0, e1;
+    DG_CUDA(cudaEventCreate(&e0));
+    DG_CUDA(cudaEventCreate(&e1));
+    const int sms = num_sms();
+    DG_CUDA(cudaEventRecord(e0, stream()));
+    if (which == 0) {
+      DevBuf<GridBarrier> b(1);
+      b.zero();
+      void* p[] = {&b.p, &iters};
+      DG_CUDA(cudaLaunchCooperativeKernel((void*)k_mb_grid, dim3(sms), dim3(1024), p, 0,
+                                          stream()));
+    } else if (which == 1) {
+      void* p[] = {&iters};
+      DG_CUDA(cudaLaunchCooperativeKernel((void*)k_mb_cg, dim3(sms), dim3(1024), p, 0, stream()));
+    } else if (which == 2) {
+      k_mb_cluster<<<8, 1024, 0, stream()>>>(iters);
+    } else if (which == 3) {
+      k_mb_bar<<<1, 1024, 0, stream()>>>(iters, sink.get());
+    } else if (which == 4 || which == 7 || which == 8) {
+      // 4 MiB (L2-resident), 64 MiB (half the L2), 1 GiB (HBM)
+      const uint32_t n = which == 4 ? (1u << 20) : which == 7 ? (1u << 24) : (1u << 28);
+      DevBuf<uint32_t> next(n);
+      k_mb_init_chase<<<256, 256, 0, stream()>>>(next.get(), n);
+      k_mb_chase<<<1, 1, 0, stream()>>>(next.get(), which == 4 ? 1000 : n / 4, sink.get());
+      DG_CUDA(cudaEventRecord(e0, stream()));
+      k_mb_chase<<<1, 1, 0, stream()>>>(next.get(), iters, sink.get());
+    } else if (which == 5 || which == 6) {
+      k_mb_atoms<<<1, 1024, 0, stream()>>>(iters, sink.get(), which == 6);
+    } else {
+      throw DgError(DG_E_PARAM, "unknown microbenchmark");
+    }
+    DG_CUDA(cudaGetLastError());
+    DG_CUDA(cudaEventRecord(e1, stream()));
+    stream_sync();
+    float ms = 0;
+    DG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    // per op: barriers per iteration; atomics per warp-instruction (32 lanes x 32 warps)
+    double ops = double(iters);
+    if (which == 5 || which == 6) ops = double(iters) * 32;  // warp instructions per SM
+    *ns_per_op = ms * 1e6 / ops;
+    return DG_OK;
+  } catch (const DgError& e) {
+    return e.code;
+  }
+}
+
+extern "C" dg_status dg_peel_profile(uint64_t out[16]) {
+  try {
+    unsigned long long o[16];
+    peel_profile(o);
+    for (int i = 0; i < 16; ++i) out[i] = o[i];
+    return DG_OK;
+  } catch (const DgError& e) {
+    return e.code;
+  }
+}

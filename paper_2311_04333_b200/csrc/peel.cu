@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
+#include "peel_kernel.cuh"
 
 namespace dgb {
 
@@ -24,161 +25,6 @@ namespace {
 
 constexpr int PT = 1024;  // peel CTA size
 constexpr size_t kSmemCap = 227 * 1024;
-
-template <class K>
-struct PeelArgs {
-  const uint64_t* offs;
-  const uint32_t* adj;
-  uint32_t n;
-  const uint64_t* loads;
-  uint64_t base;
-  int one;
-  K* gkeys;
-  uint32_t chunk;
-  uint32_t* perm;
-  uint32_t* charges;
-  unsigned long long* batches;
-};
-
-struct PeelSmem {  // fixed part, after the keys
-  uint32_t v[PT];
-  uint64_t off[PT];
-  uint64_t pre[PT];
-  uint32_t cnt[PT];
-  uint64_t ws[33];
-  uint64_t wmin[32];
-  uint32_t wcnt[32];
-};
-
-template <class K>
-__device__ __forceinline__ void key_dec(K* p);
-template <>
-__device__ __forceinline__ void key_dec<uint32_t>(uint32_t* p) {
-  atomicSub(p, 1u);
-}
-template <>
-__device__ __forceinline__ void key_dec<uint64_t>(uint64_t* p) {
-  atomicAdd(reinterpret_cast<unsigned long long*>(p), ~0ULL);
-}
-
-template <class K, bool SMEM>
-__global__ void __launch_bounds__(PT, 1) k_peel(PeelArgs<K> a) {
-  extern __shared__ __align__(16) unsigned char raw[];
-  const uint32_t npad = a.chunk * PT;
-  K* keys = SMEM ? reinterpret_cast<K*>(raw) : a.gkeys;
-  PeelSmem& s = *reinterpret_cast<PeelSmem*>(
-      raw + (SMEM ? ((size_t(npad) * sizeof(K) + 15) & ~size_t(15)) : 0));
-  const K DEAD = K(~K(0)), BATCH = K(DEAD - 1);
-  const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
-  const uint32_t n = a.n, c = a.chunk, lo = tid * c, hi = lo + c;
-
-  for (uint32_t i = lo; i < hi; ++i)
-    keys[i] = i < n ? K(a.loads[i] - a.base + (a.offs[i + 1] - a.offs[i])) : DEAD;
-  __syncthreads();
-
-  uint32_t removed = 0, pos = 0;
-  unsigned long long nbat = 0;
-  while (removed < n) {
-    // ---- S1: per-thread min over its chunk (old batch marks -> DEAD)
-    K lmin = DEAD;
-    uint32_t lcnt = 0;
-    for (uint32_t i = lo; i < hi; ++i) {
-      K k = keys[i];
-      if (k >= BATCH) {
-        if (k == BATCH) keys[i] = DEAD;
-        continue;
-      }
-      if (k < lmin) {
-        lmin = k;
-        lcnt = 1;
-      } else if (k == lmin) {
-        ++lcnt;
-      }
-    }
-    const K wm = warp_min(lmin);
-    const uint32_t contrib = (lmin == wm) ? lcnt : 0u;
-    const uint32_t incl = warp_incl_scan(contrib);
-    if (lane == 31) {
-      s.wmin[w] = uint64_t(wm);
-      s.wcnt[w] = incl;
-    }
-    __syncthreads();
-    // every warp reduces the 32 warp entries itself (no second barrier)
-    const K x = K(s.wmin[lane]);
-    const K gmin = warp_min(x);
-    const uint32_t cc = (x == gmin) ? s.wcnt[lane] : 0u;
-    const uint32_t ci = warp_incl_scan(cc);
-    const uint32_t total = __shfl_sync(0xffffffffu, ci, 31);
-    const uint32_t woff = __shfl_sync(0xffffffffu, ci - cc, w);
-    const uint32_t bs = a.one ? 1u : total;
-    // ---- S2: the batch in ascending id, straight into perm
-    if (lmin == gmin && lcnt) {
-      uint32_t my = woff + incl - contrib;
-      for (uint32_t i = lo; i < hi && my < bs; ++i)
-        if (keys[i] == gmin) {
-          a.perm[pos + my] = i;
-          keys[i] = BATCH;
-          ++my;
-        }
-    }
-    __syncthreads();
-    // ---- S3: remove the batch, slice by slice
-    for (uint32_t s0 = 0; s0 < bs; s0 += PT) {
-      const uint32_t sl = min(uint32_t(PT), bs - s0);
-      uint64_t d = 0;
-      if (tid < sl) {
-        const uint32_t v = a.perm[pos + s0 + tid];
-        const uint64_t o = a.offs[v];
-        d = a.offs[v + 1] - o;
-        s.v[tid] = v;
-        s.off[tid] = o;
-        s.cnt[tid] = 0;
-      }
-      uint64_t tot;
-      const uint64_t ex = block_excl_scan(d, s.ws, &tot);
-      s.pre[tid] = ex + d;  // inclusive
-      __syncthreads();
-      for (uint64_t b0 = tid & ~31u; b0 < tot; b0 += PT) {
-        const uint64_t x2 = b0 + lane;
-        const bool valid = x2 < tot;
-        uint32_t b = 0, cnt = 0;
-        if (valid) {
-          uint32_t l = 0, h = sl - 1;  // first b with pre[b] > x2
-          while (l < h) {
-            uint32_t mid = (l + h) >> 1;
-            if (s.pre[mid] > x2)
-              h = mid;
-            else
-              l = mid + 1;
-          }
-          b = l;
-          const uint32_t v = s.v[b];
-          const uint32_t u = a.adj[s.off[b] + (x2 - (b ? s.pre[b - 1] : 0))];
-          const K k = keys[u];
-          if (k < BATCH) {
-            key_dec<K>(&keys[u]);
-            cnt = 1;
-          } else if (k == BATCH && u > v) {
-            cnt = 1;
-          }
-        }
-        const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-          const uint32_t grp = __match_any_sync(vm, b);
-          const uint32_t sum = __popc(__ballot_sync(vm, cnt) & grp);
-          if (lane == uint32_t(__ffs(grp) - 1) && sum) atomicAdd(&s.cnt[b], sum);
-        }
-      }
-      __syncthreads();
-      if (tid < sl) a.charges[pos + s0 + tid] = s.cnt[tid];
-      __syncthreads();
-    }
-    pos += bs;
-    removed += bs;
-    ++nbat;
-  }
-  if (tid == 0) *a.batches = nbat;
-}
 
 // ---- key range: min load, max (load - min + deg)
 __global__ void k_key_range(const uint64_t* offs, const uint64_t* loads, uint64_t n,
@@ -206,7 +52,9 @@ struct A3Args {
   const uint64_t* offs;
   uint32_t n;
   const uint32_t* perm;
-  const uint32_t* A;
+  const uint32_t* A;    // final charges, or
+  const uint64_t* raw;  // raw fused-peel charges: A[i] = raw[i] - (loads[perm[i]] - base)
+  uint64_t base;
   uint64_t* loads;
   uint64_t slack_samples, slack_allowed, slack_seed;
   uint64_t* suffix;
@@ -219,6 +67,10 @@ __device__ __forceinline__ bool better(uint64_t e1, uint64_t v1, uint64_t i1, ui
   if (dens_gt(e1, v1, e2, v2)) return true;
   if (dens_gt(e2, v2, e1, v1)) return false;
   return i1 < i2;
+}
+
+__device__ __forceinline__ uint64_t charge(const A3Args& a, uint32_t i) {
+  return a.A ? uint64_t(a.A[i]) : a.raw[i] - (a.loads[a.perm[i]] - a.base);
 }
 
 __global__ void __launch_bounds__(PT, 1) k_alg3(A3Args a) {
@@ -247,9 +99,9 @@ __global__ void __launch_bounds__(PT, 1) k_alg3(A3Args a) {
   const uint32_t c = (n + blockDim.x - 1) / blockDim.x;
   const uint32_t lo = min(n, tid * c), hi = min(n, lo + c);
   uint64_t local = 0;
-  uint32_t wmax = 0;
+  uint64_t wmax = 0;
   for (uint32_t i = lo; i < hi; ++i) {
-    const uint32_t x = a.A[i];
+    const uint64_t x = charge(a, i);
     local += x;
     wmax = max(wmax, x);
   }
@@ -258,7 +110,7 @@ __global__ void __launch_bounds__(PT, 1) k_alg3(A3Args a) {
   uint64_t run = total - ex - local;  // sum of A beyond my chunk
   uint64_t be = 0, bv = 1, bi = ~0ULL;
   for (uint32_t i = hi; i-- > lo;) {
-    run += a.A[i];
+    run += charge(a, i);
     if (a.suffix) a.suffix[i] = run;
     const uint64_t d = n - i;
     if (!dens_gt(be, bv, run, d)) {  // >= : walking down, smaller i wins ties
@@ -307,7 +159,10 @@ __global__ void __launch_bounds__(PT, 1) k_alg3(A3Args a) {
     }
   }
   // loads += A (refine.cpp:213)
-  for (uint32_t i = lo; i < hi; ++i) a.loads[a.perm[i]] += a.A[i];
+  for (uint32_t i = lo; i < hi; ++i) {  // each thread owns its positions' loads
+    const uint64_t x = charge(a, i);
+    a.loads[a.perm[i]] += x;
+  }
   __syncthreads();
   // next key range over vertices
   uint64_t mn = ~0ULL;
@@ -371,22 +226,47 @@ __global__ void k_iota(uint32_t* p, uint64_t n) {
     p[i] = uint32_t(i);
 }
 
-template <class K, bool SMEM>
+unsigned long long* peel_prof_buffer() {
+  static unsigned long long* buf[64] = {};
+  int d = 0;
+  DG_CUDA(cudaGetDevice(&d));
+  if (!buf[d]) {
+    DG_CUDA(cudaMalloc(&buf[d], 16 * sizeof(unsigned long long)));
+    DG_CUDA(cudaMemset(buf[d], 0, 16 * sizeof(unsigned long long)));
+  }
+  return buf[d];
+}
+
+template <class K, bool SMEM, bool OFFS, int VQ>
 void launch_peel(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
-                 uint32_t chunk, uint32_t* d_perm, uint32_t* d_charges,
+                 uint32_t chunk, uint32_t* d_perm, uint64_t* d_raw,
                  unsigned long long* d_batches) {
   DevBuf<K> gk;
-  size_t smem = sizeof(PeelSmem);
-  if (SMEM)
-    smem += (size_t(chunk) * PT * sizeof(K) + 15) & ~size_t(15);
-  else
-    gk.alloc(size_t(chunk) * PT);
-  DG_CUDA(cudaFuncSetAttribute(k_peel<K, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
-  PeelArgs<K> a{g.offs.get(), g.adj.get(), uint32_t(g.n), d_loads, base, one ? 1 : 0,
-                gk.get(), chunk, d_perm, d_charges, d_batches};
-  k_peel<K, SMEM><<<1, PT, smem, stream()>>>(a);
+  if (!SMEM) gk.alloc(size_t(chunk) * peelk::PT);
+  const size_t smem = peelk::smem_bytes<K, OFFS>(chunk, SMEM);
+  auto kern = peelk::k_peel<K, SMEM, OFFS, VQ>;
+  DG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  peelk::Args<K> a{g.offs.get(), g.adj.get(), uint32_t(g.n), d_loads, base, one ? 1 : 0,
+                   gk.get(), chunk, d_perm, d_raw, d_batches, peel_prof_buffer()};
+  kern<<<1, peelk::PT, smem, stream()>>>(a);
   DG_CHECK_LAUNCH();
+}
+
+// u32 keys in shared memory: compile-time chunk of 4*VQ keys (VQ odd)
+template <bool OFFS>
+bool launch_vec(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one, uint32_t vq,
+                uint32_t* d_perm, uint64_t* d_raw, unsigned long long* d_batches) {
+  switch (vq) {
+#define DG_VQ(V)                                                                         \
+  case V:                                                                                \
+    launch_peel<uint32_t, true, OFFS, V>(g, d_loads, base, one, 4 * V, d_perm, d_raw,    \
+                                         d_batches);                                     \
+    return true;
+    DG_VQ(1) DG_VQ(3) DG_VQ(5) DG_VQ(7) DG_VQ(9) DG_VQ(11) DG_VQ(13)
+#undef DG_VQ
+    default:
+      return false;
+  }
 }
 
 }  // namespace
@@ -412,27 +292,51 @@ KeyRange key_range(const dg_graph& g, const uint64_t* d_loads) {
 }
 
 void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
-                bool one_at_a_time, uint32_t* d_perm, uint32_t* d_charges,
+                bool one_at_a_time, uint32_t* d_perm, uint64_t* d_raw,
                 unsigned long long* d_batches) {
   if (g.n == 0) return;
   const uint32_t n = uint32_t(g.n);
-  uint32_t chunk = (n + PT - 1) / PT;
-  chunk |= 1u;  // odd stride: conflict-free shared-memory chunk scans
-  unsigned long long* nb = d_batches;
-  const size_t fixed = sizeof(PeelSmem) + 16;
-  const bool k32 = kr.max_key < 0xfffffffdULL;
-  if (k32 && fixed + size_t(chunk) * PT * 4 <= kSmemCap)
-    launch_peel<uint32_t, true>(g, d_loads, kr.min_load, one_at_a_time, chunk, d_perm, d_charges,
-                                nb);
-  else if (!k32 && fixed + size_t(chunk) * PT * 8 <= kSmemCap)
-    launch_peel<uint64_t, true>(g, d_loads, kr.min_load, one_at_a_time, chunk, d_perm, d_charges,
-                                nb);
-  else if (k32)
-    launch_peel<uint32_t, false>(g, d_loads, kr.min_load, one_at_a_time, chunk, d_perm,
-                                 d_charges, nb);
-  else
-    launch_peel<uint64_t, false>(g, d_loads, kr.min_load, one_at_a_time, chunk, d_perm,
-                                 d_charges, nb);
+  const uint32_t per = (n + peelk::PT - 1) / peelk::PT;
+  // alive keys must stay below 2^(bits-1) and degrees below 2^28 (see the
+  // key ranges in peel_kernel.cuh)
+  if (g.maxdeg >= (1ULL << 28)) throw DgError(DG_E_PARAM, "degree too large for the peel kernel");
+  if (kr.max_key >= (1ULL << 62)) throw DgError(DG_E_PARAM, "load range exceeds 2^62");
+  const bool k32 = kr.max_key < 0x80000000ULL;
+  // u32 keys in shared memory are scanned with 128-bit loads: chunk = 4q with
+  // q odd keeps a warp's vector loads bank-conflict free; otherwise an odd
+  // chunk keeps scalar scans conflict free.
+  const uint32_t vq = ((per + 3) / 4) | 1u;
+  const uint32_t chunk_odd = per | 1u;
+  const bool offs32 = 2 * g.m < 0xffffffffULL;
+  const uint64_t base = kr.min_load;
+  if (k32) {
+    if (offs32 && peelk::smem_bytes<uint32_t, true>(4 * vq, true) <= kSmemCap &&
+        launch_vec<true>(g, d_loads, base, one_at_a_time, vq, d_perm, d_raw, d_batches))
+      return;
+    if (peelk::smem_bytes<uint32_t, false>(4 * vq, true) <= kSmemCap &&
+        launch_vec<false>(g, d_loads, base, one_at_a_time, vq, d_perm, d_raw, d_batches))
+      return;
+  }
+#define DG_PEEL_TRY(K, SM, OF)                                                               \
+  if ((sizeof(K) == 4) == k32 && (!OF || offs32) &&                                          \
+      peelk::smem_bytes<K, OF>(chunk_odd, SM) <= kSmemCap) {                                 \
+    launch_peel<K, SM, OF, 0>(g, d_loads, base, one_at_a_time, chunk_odd, d_perm, d_raw,     \
+                              d_batches);                                                    \
+    return;                                                                                  \
+  }
+  DG_PEEL_TRY(uint32_t, true, true)
+  DG_PEEL_TRY(uint32_t, true, false)
+  DG_PEEL_TRY(uint64_t, true, true)
+  DG_PEEL_TRY(uint64_t, true, false)
+  DG_PEEL_TRY(uint32_t, false, false)
+  DG_PEEL_TRY(uint64_t, false, false)
+#undef DG_PEEL_TRY
+  throw DgError(DG_E_INVARIANT, "no peel kernel variant fits");
+}
+
+void peel_profile(unsigned long long out[16]) {
+  d2h(out, peel_prof_buffer(), 16);
+  stream_sync();
 }
 
 void sort_order(uint64_t n, const uint64_t* d_loads, uint32_t* d_perm) {
@@ -465,10 +369,12 @@ void charges_from_perm(const dg_graph& g, const uint32_t* d_perm, uint32_t* d_ch
   DG_CHECK_LAUNCH();
 }
 
-void alg3(const dg_graph& g, const uint32_t* d_perm, const uint32_t* d_charges, uint64_t* d_loads,
+void alg3(const dg_graph& g, const uint32_t* d_perm, const uint32_t* d_charges,
+          const uint64_t* d_raw, uint64_t raw_base, uint64_t* d_loads,
           uint64_t slack_samples, uint64_t slack_allowed, uint64_t slack_seed, uint64_t* d_suffix,
           Alg3Out* d_out) {
-  A3Args a{g.offs.get(), uint32_t(g.n), d_perm, d_charges, d_loads, slack_samples, slack_allowed,
+  A3Args a{g.offs.get(), uint32_t(g.n), d_perm, d_charges, d_raw, raw_base, d_loads,
+           slack_samples, slack_allowed,
            slack_seed, d_suffix, d_out};
   k_alg3<<<1, PT, 0, stream()>>>(a);
   DG_CHECK_LAUNCH();

@@ -1,0 +1,414 @@
+// peel_kernel.cuh -- the Greedy++ batch-peel kernel (one CTA, whole chain).
+//
+// Reference semantics: refine.cpp:20-156 (PeelState / peel_buckets /
+// peel_heap): key = load + residual degree; a batch is EVERY alive vertex at
+// the exact minimum key, in ascending id; batch members die before any
+// decrement; each alive neighbour loses one key unit per removed neighbour.
+//
+// Fused Algorithm 3 charge (refine.cpp:195-199).  A[pos(v)] counts v's
+// neighbours positioned after v: alive after v's batch, or in v's batch with
+// a larger id.  At removal key(v) = load(v) + #neighbours alive at that
+// moment (same-batch members included), so
+//     A[pos(v)] = key_at_removal(v) - load(v) - #same-batch neighbours u < v.
+// The kernel emits raw[pos] = key_at_removal - #smaller same-batch
+// neighbours, and Alg. 3 subtracts the load.
+//
+// Key ranges instead of sentinels.  Alive keys live in [0, 2^(b-1)); a batch
+// member is re-keyed to BATCH = 3*2^(b-2) - 1, a removed vertex to DEAD =
+// 2^b - 1.  A vertex receives fewer than 2^28 decrements (its degree), so
+// decremented marks stay inside [2^(b-1), 3*2^(b-2)) resp. [3*2^(b-2), 2^b):
+// removal decrements EVERY neighbour unconditionally (red.shared.add, or
+// atom.shared.add whose return value tells batch members apart) and the min
+// scan ignores non-alive keys for free (they are the largest values).
+//
+// The kernel is issue-bound (32 warps share 4 schedulers), so every phase is
+// written for instruction count:
+//   S1  each thread scans its contiguous chunk of 4*VQ keys with 128-bit
+//       shared loads (VQ odd: conflict free, fully unrolled at compile time):
+//       3-input min, then the multiplicity; redux.sync -> 32-entry warp table
+//   --- barrier A
+//   S2  every warp reduces the table with redux.sync (global min, batch size,
+//       its output offset); owners of the minimum write the batch in
+//       ascending id into perm and stage (v, row offset, degree)
+//   --- barrier B
+//   S3  the batch's rows are cut into 16-byte adjacency quads; a flat quad
+//       index is spread over the CTA (U quads in flight per thread), each
+//       quad = one 128-bit load + four shared reductions.  Batches > 32
+//       members take a slice path with a CTA scan.
+//   --- barrier C
+//   raw charges of the batch are written to global at the next S1.
+#pragma once
+
+namespace dgb {
+namespace peelk {
+
+constexpr int PT = 1024;  // threads
+constexpr int U = 4;      // arcs in flight per thread (large-batch path)
+constexpr int UQ = 2;     // adjacency quads in flight per thread (small-batch path)
+
+template <class K>
+struct Args {
+  const uint64_t* offs;
+  const uint32_t* adj;
+  uint32_t n;
+  const uint64_t* loads;
+  uint64_t base;
+  int one;
+  K* gkeys;  // keys in global memory when they do not fit in shared
+  uint32_t chunk;
+  uint32_t* perm;
+  uint64_t* raw;                // raw charges per position (see header)
+  unsigned long long* batches;
+  unsigned long long* prof;     // [8] thread-0 cycles S1,S2,S3, batches, S3 of 1-vertex batches, #1-vertex, #>32, n
+};
+
+struct Fixed {  // shared-memory tail after keys (and offsets)
+  uint32_t bv[PT];
+  uint64_t boff[PT];
+  uint32_t bdeg[PT];
+  uint32_t cnt[PT];
+  uint64_t pre[PT];
+  uint64_t ws[33];
+  uint64_t wmin[32];
+  uint32_t wcnt[32];
+};
+
+template <class K>
+struct Range {
+  static constexpr K ALIVE_END = K(K(1) << (8 * sizeof(K) - 1));  // 2^(b-1)
+  static constexpr K DEAD_LO = K(ALIVE_END | (ALIVE_END >> 1));   // 3*2^(b-2)
+  static constexpr K BATCH = K(DEAD_LO - 1);
+  static constexpr K DEAD = K(~K(0));
+  __device__ static bool alive(K k) { return k < ALIVE_END; }
+  __device__ static bool in_batch(K k) { return k >= ALIVE_END && k < DEAD_LO; }
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+// decrement without return
+__device__ __forceinline__ void key_red(uint32_t* p, bool smem) {
+  if (smem)
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(0xffffffffu) : "memory");
+  else
+    atomicAdd(p, 0xffffffffu);
+}
+__device__ __forceinline__ void key_red(uint64_t* p, bool smem) {
+  if (smem)
+    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(smem_addr(p)), "l"(~0ULL) : "memory");
+  else
+    atomicAdd(reinterpret_cast<unsigned long long*>(p), ~0ULL);
+}
+// decrement returning the old key
+__device__ __forceinline__ uint32_t key_atom(uint32_t* p) { return atomicAdd(p, 0xffffffffu); }
+__device__ __forceinline__ uint64_t key_atom(uint64_t* p) {
+  return atomicAdd(reinterpret_cast<unsigned long long*>(p), ~0ULL);
+}
+
+// warp-wide min of a key (redux.sync for 32-bit keys)
+__device__ __forceinline__ uint32_t wmin_key(uint32_t x) { return __reduce_min_sync(~0u, x); }
+__device__ __forceinline__ uint64_t wmin_key(uint64_t x) { return warp_min(x); }
+
+// S1 over a compile-time chunk of 4*VQ u32 keys (VQ > 0) or a runtime chunk.
+template <int VQ, class K>
+__device__ __forceinline__ void chunk_min_count(const K* keys, uint32_t lo, uint32_t c, K& lmin,
+                                                uint32_t& lcnt) {
+  if constexpr (VQ > 0 && sizeof(K) == 4) {
+    const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
+    uint32_t m = 0xffffffffu;
+#pragma unroll
+    for (int q = 0; q < VQ; ++q) {
+      const uint4 v = kv[q];
+      m = min(min(m, min(v.x, v.y)), min(v.z, v.w));
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int q = 0; q < VQ; ++q) {
+      const uint4 v = kv[q];
+      cnt += uint32_t(v.x == m) + uint32_t(v.y == m) + uint32_t(v.z == m) + uint32_t(v.w == m);
+    }
+    lmin = K(m);
+    lcnt = cnt;
+  } else {
+    K m = K(~K(0));
+    for (uint32_t i = lo; i < lo + c; ++i) m = min(m, keys[i]);
+    uint32_t cnt = 0;
+    for (uint32_t i = lo; i < lo + c; ++i) cnt += keys[i] == m;
+    lmin = m;
+    lcnt = cnt;
+  }
+}
+
+template <class K, bool SMEM, bool OFFS, int VQ>
+__global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
+  using R = Range<K>;
+  extern __shared__ __align__(16) unsigned char raw_smem[];
+  const uint32_t npad = a.chunk * PT;
+  size_t o = 0;
+  K* keys = a.gkeys;
+  if (SMEM) {
+    keys = reinterpret_cast<K*>(raw_smem);
+    o = (size_t(npad) * sizeof(K) + 15) & ~size_t(15);
+  }
+  uint32_t* soffs = reinterpret_cast<uint32_t*>(raw_smem + o);  // u32 row starts, n+1
+  if (OFFS) o += (size_t(npad + 1) * 4 + 15) & ~size_t(15);
+  Fixed& s = *reinterpret_cast<Fixed*>(raw_smem + o);
+  const uint4* adj4 = reinterpret_cast<const uint4*>(a.adj);
+
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
+  const uint32_t n = a.n, c = VQ > 0 ? uint32_t(4 * VQ) : a.chunk, lo = tid * c, hi = lo + c;
+
+  for (uint32_t i = lo; i < hi; ++i) {
+    if (i < n) {
+      const uint64_t o0 = a.offs[i], o1 = a.offs[i + 1];
+      keys[i] = K(a.loads[i] - a.base + (o1 - o0));
+      if (OFFS) soffs[i] = uint32_t(o0);
+    } else {
+      keys[i] = R::DEAD;
+    }
+  }
+  if (OFFS && tid == 0) soffs[n] = uint32_t(a.offs[n]);
+  __syncthreads();
+
+  uint32_t removed = 0, pos = 0, pend_n = 0, pend_pos = 0;
+  K pend_key = 0;
+  bool marked = false;  // this thread holds BATCH marks of the previous batch
+  unsigned long long nbat = 0;
+  long long c_s1 = 0, c_s2 = 0, c_s3 = 0, c_s3_1 = 0, t_mark = clock64();
+  unsigned long long n1 = 0, nbig = 0;
+  long long d1 = 0, d2 = 0, d3 = 0, tq = 0;
+  while (removed < n) {
+    // ---- deferred raw charges of the previous batch
+    if (tid < pend_n) a.raw[pend_pos + tid] = uint64_t(pend_key) - s.cnt[tid];
+    // ---- S1
+    K lmin;
+    uint32_t lcnt;
+    chunk_min_count<VQ>(keys, lo, c, lmin, lcnt);
+    if (!R::alive(lmin)) {  // nothing alive in my chunk
+      lmin = R::DEAD;
+      lcnt = 0;
+    }
+    const K wm = wmin_key(lmin);
+    const uint32_t wc = __reduce_add_sync(~0u, lmin == wm ? lcnt : 0u);
+    if (lane == 0) {
+      s.wmin[w] = uint64_t(wm);
+      s.wcnt[w] = wc;
+    }
+    __syncthreads();  // A
+    if (tid == 0) {
+      const long long t = clock64();
+      c_s1 += t - t_mark;
+      t_mark = t;
+    }
+    // ---- S2: global min, batch size, output offsets; write the batch
+    const K xw = K(s.wmin[lane]);
+    const K gmin = wmin_key(xw);
+    const uint32_t cc = (xw == gmin) ? s.wcnt[lane] : 0u;
+    const uint32_t total = __reduce_add_sync(~0u, cc);
+    const uint32_t bs = a.one ? 1u : total;
+    if (marked) {  // retire my marks of the previous batch
+      for (uint32_t i = lo; i < hi; ++i)
+        if (R::in_batch(keys[i])) keys[i] = R::DEAD;
+      marked = false;
+    }
+    if (wm == gmin) {  // this warp owns part of the batch
+      const uint32_t woff = __reduce_add_sync(~0u, lane < w ? cc : 0u);
+      const bool mine = lmin == gmin && lcnt;
+      const uint32_t mm = __ballot_sync(~0u, mine);
+      uint32_t my = woff;
+      if (__popc(mm) > 1) {  // several owners in this warp: lane prefix of counts
+        const uint32_t v = mine ? lcnt : 0u;
+        my += warp_incl_scan(v) - v;
+      }
+      if (mine) {
+        for (uint32_t i = lo; i < hi && my < bs; ++i) {
+          if (keys[i] != gmin) continue;
+          a.perm[pos + my] = i;
+          // a single-vertex batch has no same-batch arcs: mark it dead at once
+          keys[i] = bs == 1 ? R::DEAD : R::BATCH;
+          marked = bs != 1;
+          if (my < PT) {
+            uint64_t r0, r1;
+            if (OFFS) {
+              r0 = soffs[i];
+              r1 = soffs[i + 1];
+            } else {
+              r0 = a.offs[i];
+              r1 = a.offs[i + 1];
+            }
+            s.bv[my] = i;
+            s.boff[my] = r0;
+            s.bdeg[my] = uint32_t(r1 - r0);
+            s.cnt[my] = 0;
+          }
+          ++my;
+        }
+      }
+    }
+    __syncthreads();  // B
+    if (tid == 0) {
+      const long long t = clock64();
+      c_s2 += t - t_mark;
+      t_mark = t;
+    }
+    if (bs <= 32) {
+      // ---- S3: rows cut into 16-byte quads, flat quad index over the CTA
+      const uint64_t ol = lane < bs ? s.boff[lane] : 0;
+      const uint64_t el = ol + (lane < bs ? s.bdeg[lane] : 0u);
+      const uint32_t vl = lane < bs ? s.bv[lane] : 0u;
+      const uint32_t nql = lane < bs ? uint32_t(((el + 3) >> 2) - (ol >> 2)) : 0u;
+      const uint32_t incq = bs == 1 ? nql : warp_incl_scan(nql);
+      const uint32_t totq = __shfl_sync(~0u, incq, bs - 1);
+      const uint32_t exq = incq - nql;
+      if (tid == 0) tq = clock64();
+      for (uint32_t base = w * 32; base < totq; base += PT * UQ) {
+        uint32_t b[UQ], f[UQ];
+#pragma unroll
+        for (int k = 0; k < UQ; ++k) {
+          f[k] = base + k * PT + lane;
+          b[k] = 0;
+        }
+        if (bs > 1) {
+          for (uint32_t mb = 1; mb < bs; ++mb) {
+            const uint32_t e = __shfl_sync(~0u, exq, mb);
+#pragma unroll
+            for (int k = 0; k < UQ; ++k)
+              if (f[k] >= e) b[k] = mb;
+          }
+        }
+        uint4 x[UQ];
+        uint64_t p0[UQ], lo_b[UQ], hi_b[UQ];
+        uint32_t v_b[UQ];
+#pragma unroll
+        for (int k = 0; k < UQ; ++k) {
+          lo_b[k] = __shfl_sync(~0u, ol, b[k]);
+          hi_b[k] = __shfl_sync(~0u, el, b[k]);
+          v_b[k] = __shfl_sync(~0u, vl, b[k]);
+          const uint32_t ex = __shfl_sync(~0u, exq, b[k]);
+          const uint64_t q = (lo_b[k] >> 2) + (f[k] - ex);
+          p0[k] = q << 2;
+          if (f[k] < totq) x[k] = __ldg(adj4 + q);
+        }
+        if (tid == 0) {
+          const long long t = clock64();
+          d1 += t - tq;
+          tq = t;
+        }
+#pragma unroll
+        for (int k = 0; k < UQ; ++k) {
+          if (f[k] >= totq) continue;
+          const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint64_t p = p0[k] + e;
+            if (p < lo_b[k] || p >= hi_b[k]) continue;
+            if (bs == 1) {
+              key_red(&keys[us[e]], SMEM);
+            } else {
+              const K old = key_atom(&keys[us[e]]);
+              if (R::in_batch(old) && us[e] < v_b[k]) atomicAdd(&s.cnt[b[k]], 1u);
+            }
+          }
+        }
+      }
+      if (tid == 0) {
+        const long long t = clock64();
+        d2 += t - tq;
+        tq = t;
+      }
+      __syncthreads();  // C
+      if (tid == 0) d3 += clock64() - tq;
+      pend_n = bs;
+      pend_pos = pos;
+      pend_key = gmin;
+    } else {
+      // ---- S3, large batch: slices of PT members with a CTA scan
+      for (uint32_t s0 = 0; s0 < bs; s0 += PT) {
+        const uint32_t sl = min(uint32_t(PT), bs - s0);
+        if (s0 > 0 && tid < sl) {  // beyond the staged first slice
+          const uint32_t v = a.perm[pos + s0 + tid];
+          const uint64_t r0 = a.offs[v], r1 = a.offs[v + 1];
+          s.bv[tid] = v;
+          s.boff[tid] = r0;
+          s.bdeg[tid] = uint32_t(r1 - r0);
+          s.cnt[tid] = 0;
+        }
+        __syncthreads();
+        const uint64_t d = tid < sl ? s.bdeg[tid] : 0;
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(d, s.ws, &tot);
+        s.pre[tid] = ex + d;
+        __syncthreads();
+        for (uint64_t b0 = uint64_t(w) * 32 * U; b0 < tot; b0 += uint64_t(PT) * U) {
+          uint32_t u[U], bb[U];
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const uint64_t x = b0 + uint64_t(j) * 32 + lane;
+            u[j] = 0xffffffffu;
+            bb[j] = 0;
+            if (x < tot) {
+              uint32_t l = 0, h = sl - 1;
+              while (l < h) {
+                const uint32_t mid = (l + h) >> 1;
+                if (s.pre[mid] > x)
+                  h = mid;
+                else
+                  l = mid + 1;
+              }
+              bb[j] = l;
+              u[j] = a.adj[s.boff[l] + (x - (l ? s.pre[l - 1] : 0))];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            if (u[j] == 0xffffffffu) continue;
+            const K old = key_atom(&keys[u[j]]);
+            if (R::in_batch(old) && u[j] < s.bv[bb[j]]) atomicAdd(&s.cnt[bb[j]], 1u);
+          }
+        }
+        __syncthreads();
+        if (tid < sl) a.raw[pos + s0 + tid] = uint64_t(gmin) - s.cnt[tid];
+        __syncthreads();
+      }
+      pend_n = 0;
+    }
+    if (tid == 0) {
+      const long long t = clock64();
+      c_s3 += t - t_mark;
+      if (bs == 1) c_s3_1 += t - t_mark, ++n1;
+      if (bs > 32) ++nbig;
+      t_mark = t;
+    }
+    pos += bs;
+    removed += bs;
+    ++nbat;
+  }
+  if (tid < pend_n) a.raw[pend_pos + tid] = uint64_t(pend_key) - s.cnt[tid];
+  if (tid == 0) {
+    *a.batches = nbat;
+    if (a.prof) {
+      a.prof[0] = c_s1;
+      a.prof[1] = c_s2;
+      a.prof[2] = c_s3;
+      a.prof[3] = nbat;
+      a.prof[4] = c_s3_1;
+      a.prof[5] = n1;
+      a.prof[6] = nbig;
+      a.prof[7] = removed;
+      a.prof[8] = d1;
+      a.prof[9] = d2;
+      a.prof[10] = d3;
+    }
+  }
+}
+
+template <class K, bool OFFS>
+size_t smem_bytes(uint32_t chunk, bool in_smem) {
+  const size_t npad = size_t(chunk) * PT;
+  size_t b = in_smem ? ((npad * sizeof(K) + 15) & ~size_t(15)) : 0;
+  if (OFFS) b += ((npad + 1) * 4 + 15) & ~size_t(15);
+  return b + sizeof(Fixed);
+}
+
+}  // namespace peelk
+}  // namespace dgb

@@ -1,0 +1,19 @@
+"""Latency floors on this B200 (dg_microbench): python tools/microbench.py"""
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2311_04333_b200 as dg  # noqa: E402
+
+NAMES = ["grid_barrier_ns", "cg_grid_sync_ns", "cluster8_sync_ns", "cta_syncthreads_ns",
+         "dependent_load_4MiB_ns", "smem_atomic_per_warp_instr_ns",
+         "smem_plain_rmw_per_warp_instr_ns", "dependent_load_64MiB_ns", "dependent_load_1GiB_ns"]
+ITERS = [20000, 20000, 100000, 1000000, 200000, 20000, 20000, 200000, 100000]
+out = {}
+for i, (name, it) in enumerate(zip(NAMES, ITERS)):
+    ns = C.c_double()
+    st = dg.LIB.dg_microbench(i, it, C.byref(ns))
+    out[name] = round(ns.value, 2) if st == 0 else f"error {st}: {dg.LIB.dg_last_error().decode()}"
+print(json.dumps(out))
