@@ -71,6 +71,10 @@ struct Fixed {  // shared-memory tail after keys (and offsets)
   uint64_t ws[33];
   uint64_t wmin[32];
   uint32_t wcnt[32];
+  // warp -> member assignment for batches of 1..32 members:
+  // wmap[bs-1][w] = j | rank << 8 | nwj << 16 with j = w % bs, rank = w / bs,
+  // nwj = #warps serving member j (precomputed: no runtime division)
+  uint32_t wmap[32][PT / 32];
 };
 
 template <class K>
@@ -168,6 +172,11 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
     }
   }
   if (OFFS && tid == 0) soffs[n] = uint32_t(a.offs[n]);
+  for (uint32_t e = tid; e < 32 * (PT / 32); e += PT) {
+    const uint32_t b = e / (PT / 32) + 1, ww = e % (PT / 32);
+    const uint32_t jj = ww % b;
+    s.wmap[b - 1][ww] = jj | ((ww / b) << 8) | (((PT / 32 - 1 - jj) / b + 1) << 16);
+  }
   __syncthreads();
 
   uint32_t removed = 0, pos = 0, pend_n = 0, pend_pos = 0;
@@ -176,7 +185,6 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
   unsigned long long nbat = 0;
   long long c_s1 = 0, c_s2 = 0, c_s3 = 0, c_s3_1 = 0, t_mark = clock64();
   unsigned long long n1 = 0, nbig = 0;
-  long long d1 = 0, d2 = 0, d3 = 0, tq = 0;
   while (removed < n) {
     // ---- deferred raw charges of the previous batch
     if (tid < pend_n) a.raw[pend_pos + tid] = uint64_t(pend_key) - s.cnt[tid];
@@ -184,6 +192,22 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
     K lmin;
     uint32_t lcnt;
     chunk_min_count<VQ>(keys, lo, c, lmin, lcnt);
+    // Without staged offsets, prefetch the row bounds of my chunk's first
+    // minimum now: if this thread owns the batch, the L2 round trip has
+    // already overlapped barrier A.
+    uint32_t pf_i = 0xffffffffu;
+    uint64_t pf0 = 0, pf1 = 0;
+    if (!OFFS && R::alive(lmin)) {
+      for (uint32_t i = lo; i < hi; ++i)
+        if (keys[i] == lmin) {
+          pf_i = i;
+          break;
+        }
+      if (pf_i != 0xffffffffu) {
+        pf0 = a.offs[pf_i];
+        pf1 = a.offs[pf_i + 1];
+      }
+    }
     if (!R::alive(lmin)) {  // nothing alive in my chunk
       lmin = R::DEAD;
       lcnt = 0;
@@ -201,14 +225,32 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
       t_mark = t;
     }
     // ---- S2: global min, batch size, output offsets; write the batch
-    const K xw = K(s.wmin[lane]);
+    constexpr uint32_t NW = PT / 32;
+    const K xw = lane < NW ? K(s.wmin[lane]) : Range<K>::DEAD;
     const K gmin = wmin_key(xw);
-    const uint32_t cc = (xw == gmin) ? s.wcnt[lane] : 0u;
+    const uint32_t cc = (lane < NW && xw == gmin) ? s.wcnt[lane] : 0u;
     const uint32_t total = __reduce_add_sync(~0u, cc);
     const uint32_t bs = a.one ? 1u : total;
     if (marked) {  // retire my marks of the previous batch
-      for (uint32_t i = lo; i < hi; ++i)
-        if (R::in_batch(keys[i])) keys[i] = R::DEAD;
+      if constexpr (VQ > 0 && sizeof(K) == 4) {
+        uint4* kv = reinterpret_cast<uint4*>(keys) + (lo >> 2);
+#pragma unroll
+        for (int q = 0; q < VQ; ++q) {
+          uint4 v = kv[q];
+          const bool hit = R::in_batch(K(v.x)) | R::in_batch(K(v.y)) | R::in_batch(K(v.z)) |
+                           R::in_batch(K(v.w));
+          if (hit) {
+            if (R::in_batch(K(v.x))) v.x = uint32_t(R::DEAD);
+            if (R::in_batch(K(v.y))) v.y = uint32_t(R::DEAD);
+            if (R::in_batch(K(v.z))) v.z = uint32_t(R::DEAD);
+            if (R::in_batch(K(v.w))) v.w = uint32_t(R::DEAD);
+            kv[q] = v;
+          }
+        }
+      } else {
+        for (uint32_t i = lo; i < hi; ++i)
+          if (R::in_batch(keys[i])) keys[i] = R::DEAD;
+      }
       marked = false;
     }
     if (wm == gmin) {  // this warp owns part of the batch
@@ -221,8 +263,33 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
         my += warp_incl_scan(v) - v;
       }
       if (mine) {
-        for (uint32_t i = lo; i < hi && my < bs; ++i) {
-          if (keys[i] != gmin) continue;
+        // owner: the chunk's minima in ascending id.  With compile-time chunks
+        // the 128-bit loads are issued up front and matches become a bitmask.
+        uint64_t bits = 0;
+        if constexpr (VQ > 0 && sizeof(K) == 4) {
+          const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
+#pragma unroll
+          for (int q = 0; q < VQ; ++q) {
+            const uint4 v = kv[q];
+            bits |= uint64_t((v.x == gmin) | ((v.y == gmin) << 1) | ((v.z == gmin) << 2) |
+                             ((v.w == gmin) << 3))
+                    << (4 * q);
+          }
+        } else {
+          for (uint32_t i = lo; i < hi && i - lo < 64; ++i)
+            if (keys[i] == gmin) bits |= 1ULL << (i - lo);
+        }
+        uint32_t i_scalar = lo + 64;  // chunks longer than 64 keys continue scalar
+        while (my < bs) {
+          uint32_t i;
+          if (bits) {
+            i = lo + uint32_t(__ffsll(bits) - 1);
+            bits &= bits - 1;
+          } else {
+            while (i_scalar < hi && keys[i_scalar] != gmin) ++i_scalar;
+            if (i_scalar >= hi) break;
+            i = i_scalar++;
+          }
           a.perm[pos + my] = i;
           // a single-vertex batch has no same-batch arcs: mark it dead at once
           keys[i] = bs == 1 ? R::DEAD : R::BATCH;
@@ -232,6 +299,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
             if (OFFS) {
               r0 = soffs[i];
               r1 = soffs[i + 1];
+            } else if (i == pf_i) {
+              r0 = pf0;
+              r1 = pf1;
             } else {
               r0 = a.offs[i];
               r1 = a.offs[i + 1];
@@ -252,72 +322,40 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
       t_mark = t;
     }
     if (bs <= 32) {
-      // ---- S3: rows cut into 16-byte quads, flat quad index over the CTA
-      const uint64_t ol = lane < bs ? s.boff[lane] : 0;
-      const uint64_t el = ol + (lane < bs ? s.bdeg[lane] : 0u);
-      const uint32_t vl = lane < bs ? s.bv[lane] : 0u;
-      const uint32_t nql = lane < bs ? uint32_t(((el + 3) >> 2) - (ol >> 2)) : 0u;
-      const uint32_t incq = bs == 1 ? nql : warp_incl_scan(nql);
-      const uint32_t totq = __shfl_sync(~0u, incq, bs - 1);
-      const uint32_t exq = incq - nql;
-      if (tid == 0) tq = clock64();
-      for (uint32_t base = w * 32; base < totq; base += PT * UQ) {
-        uint32_t b[UQ], f[UQ];
-#pragma unroll
-        for (int k = 0; k < UQ; ++k) {
-          f[k] = base + k * PT + lane;
-          b[k] = 0;
-        }
-        if (bs > 1) {
-          for (uint32_t mb = 1; mb < bs; ++mb) {
-            const uint32_t e = __shfl_sync(~0u, exq, mb);
-#pragma unroll
-            for (int k = 0; k < UQ; ++k)
-              if (f[k] >= e) b[k] = mb;
-          }
-        }
+      // ---- S3: warp w serves member j = w mod bs (warp-uniform), its lanes
+      // walk the member's row in 16-byte quads: no prefix scan, no search,
+      // the row bounds are broadcast shared loads.
+      const uint32_t wm3 = s.wmap[bs - 1][w];
+      const uint32_t j = wm3 & 0xffu, rank = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
+      const uint64_t oj = s.boff[j], ej = oj + s.bdeg[j];
+      const uint32_t vj = s.bv[j];
+      const uint64_t q1 = (ej + 3) >> 2, stride = uint64_t(nwj) * 32;
+      for (uint64_t base = (oj >> 2) + uint64_t(rank) * 32; base < q1; base += stride * UQ) {
         uint4 x[UQ];
-        uint64_t p0[UQ], lo_b[UQ], hi_b[UQ];
-        uint32_t v_b[UQ];
 #pragma unroll
         for (int k = 0; k < UQ; ++k) {
-          lo_b[k] = __shfl_sync(~0u, ol, b[k]);
-          hi_b[k] = __shfl_sync(~0u, el, b[k]);
-          v_b[k] = __shfl_sync(~0u, vl, b[k]);
-          const uint32_t ex = __shfl_sync(~0u, exq, b[k]);
-          const uint64_t q = (lo_b[k] >> 2) + (f[k] - ex);
-          p0[k] = q << 2;
-          if (f[k] < totq) x[k] = __ldg(adj4 + q);
-        }
-        if (tid == 0) {
-          const long long t = clock64();
-          d1 += t - tq;
-          tq = t;
+          const uint64_t q = base + k * stride + lane;
+          if (q < q1) x[k] = __ldg(adj4 + q);
         }
 #pragma unroll
         for (int k = 0; k < UQ; ++k) {
-          if (f[k] >= totq) continue;
+          const uint64_t q = base + k * stride + lane;
+          if (q >= q1) continue;
           const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const uint64_t p = p0[k] + e;
-            if (p < lo_b[k] || p >= hi_b[k]) continue;
+            const uint64_t p = (q << 2) + e;
+            if (p < oj || p >= ej) continue;
             if (bs == 1) {
               key_red(&keys[us[e]], SMEM);
-            } else {
+            } else {  // the returned key tells same-batch neighbours apart
               const K old = key_atom(&keys[us[e]]);
-              if (R::in_batch(old) && us[e] < v_b[k]) atomicAdd(&s.cnt[b[k]], 1u);
+              if (R::in_batch(old) && us[e] < vj) atomicAdd(&s.cnt[j], 1u);
             }
           }
         }
       }
-      if (tid == 0) {
-        const long long t = clock64();
-        d2 += t - tq;
-        tq = t;
-      }
       __syncthreads();  // C
-      if (tid == 0) d3 += clock64() - tq;
       pend_n = bs;
       pend_pos = pos;
       pend_key = gmin;
@@ -395,9 +433,6 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
       a.prof[5] = n1;
       a.prof[6] = nbig;
       a.prof[7] = removed;
-      a.prof[8] = d1;
-      a.prof[9] = d2;
-      a.prof[10] = d3;
     }
   }
 }

@@ -30,5 +30,3 @@ print(f"last peel launch: batches={prof[3]} cycles/batch S1={prof[0]/max(1,prof[
       f"(split {100*prof[0]/tot:.0f}/{100*prof[1]/tot:.0f}/{100*prof[2]/tot:.0f}%) "
       f"single-vertex batches={prof[5]} S3/single={prof[4]/max(1,prof[5]):.0f} "
       f"S3/multi={(prof[2]-prof[4])/max(1,prof[3]-prof[5]):.0f} big={prof[6]}")
-nb = max(1, prof[3] - prof[6])
-print(f"  thread0 S3 small path: pre-load={prof[8]/nb:.0f} load+process={prof[9]/nb:.0f} barrierC={prof[10]/nb:.0f} cycles/batch")
