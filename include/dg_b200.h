@@ -208,6 +208,10 @@ dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op);
  * S1 (min scan), S2 (batch extraction), S3 (removal), its batch count, S3
  * cycles of single-vertex batches, their count, #batches > 32, n. */
 dg_status dg_peel_profile(uint64_t out[16]);
+/* Diagnostic: block-0 cycles of the last coreness launch in level-advance min
+ * scans, level-advance barriers, collects, expansion, flushes, expansion
+ * barriers; #level advances; #overflow collects. */
+dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]);  /* + per-round trace */
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,7 @@ PROTOTYPES = {
     "dg_flush_l2": (C.c_int, []),
     "dg_microbench": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_double)]),
     "dg_peel_profile": (C.c_int, [u64p]),
+    "dg_kcore_profile": (C.c_int, [u64p]),
 }
 
 

@@ -246,8 +246,11 @@ __device__ __forceinline__ bool grid_sync(GridBarrier* b, uint32_t nblocks, uint
     // barrier episode is exactly 2^31.  Waiters poll the same word; no reset
     // store, one atomic round trip on the critical path.
     const uint32_t add = blockIdx.x == 0 ? 0x80000000u - (nblocks - 1) : 1u;
-    __threadfence();
-    const uint32_t old = atomicAdd(&b->count, add);
+    uint32_t old;  // release-ordered arrival, acquire-ordered polling: no full fences
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;"
+                 : "=r"(old)
+                 : "l"(&b->count), "r"(add)
+                 : "memory");
     const long long t0 = clock64();
     uint32_t spins = 0;
     while (((old ^ ld_acquire_u32(&b->count)) & 0x80000000u) == 0) {
@@ -259,7 +262,6 @@ __device__ __forceinline__ bool grid_sync(GridBarrier* b, uint32_t nblocks, uint
         }
       }
     }
-    __threadfence();
     *s_abort = ld_relaxed_u32(&b->abort);
     fetch();
   }

@@ -12,19 +12,22 @@
 // B200 mapping:
 //   * frontier of round r+1 = vertices whose degree crossed b+1 -> b during
 //     round r, detected by the atomicSub return value (no bucket rescans);
-//   * frontier entries carry an exclusive arc prefix, and a "chunk-start"
-//     table cse[c] = entry holding arc c*CH, so the expansion is perfectly
-//     load balanced over warps (hub rows are spread over many warps) with
-//     one coalesced adjacency pass;
-//   * appends are aggregated in shared memory and published with ONE packed
-//     64-bit atomic per CTA per tile: (count << 36) | arcs;  a CTA whose
-//     buffer overflows leaves the vertex unlabelled and raises a flag, and an
-//     extra collect phase picks those up from the live list;
+//   * a frontier entry is (vertex, exclusive arc prefix, row offset), and a
+//     chunk-start table cse[c] = entry holding arc 32c makes the expansion
+//     perfectly load balanced: one warp step = 32 consecutive arcs; the step
+//     loads its <= 32 entry starts coalesced and finds each lane's entry with
+//     a 5-step shuffle search (no memory in the dependent chain).  Each warp
+//     keeps UC steps in flight, so hub rows are spread over many warps and
+//     small rows are packed 32 arcs per step;
+//   * crossings are buffered in shared memory and published with ONE packed
+//     64-bit atomic per CTA per tile: (count << 36) | arcs; a CTA whose buffer
+//     overflows leaves the vertex unlabelled and raises a flag, and an extra
+//     collect phase picks those up from the live list;
 //   * the live list (alive vertices) is compacted at every level advance, so
 //     min-degree scans shrink with the graph;
-//   * one generation barrier per round (two per level advance).
-#include <cooperative_groups.h>
-
+//   * one grid barrier per round (two per level advance); only thread 0 of a
+//     CTA touches the barrier and the phase scalars (fetched into shared
+//     memory), so no L2 line is hammered by the whole grid.
 #include "internal.cuh"
 
 namespace dgb {
@@ -32,16 +35,24 @@ namespace dgb {
 namespace {
 
 constexpr int KC_THREADS = 1024;
-constexpr uint32_t CH = 128;   // arcs per warp work chunk (4 per lane)
-constexpr uint32_t BUF = 6144; // per-CTA crossing buffer
+constexpr uint32_t CH = 32;     // arcs per chunk = one warp step
+constexpr int UC = 2;           // chunks in flight per warp
+constexpr uint32_t BUF = 4096;  // per-CTA crossing buffer
 constexpr uint32_t kUnset = 0xffffffffu;
 constexpr uint64_t M36 = (1ULL << 36) - 1;
 
-struct Acc {
+struct alignas(128) Acc {  // one cache line each: no false sharing between phases
   unsigned long long front;  // (count << 36) | arcs of the frontier being built
   unsigned long long live;   // live-list entries written
   uint32_t minv;             // min alive degree (level advance)
   uint32_t ovf;              // some CTA buffer overflowed while building
+};
+
+struct Frontier {
+  uint32_t* v;    // vertex
+  uint64_t* fa;   // exclusive arc prefix
+  uint64_t* fo;   // row offset offs[v]
+  uint32_t* cse;  // cse[c] = entry holding arc CH*c
 };
 
 struct KcArgs {
@@ -52,15 +63,12 @@ struct KcArgs {
   uint32_t* labels;
   uint32_t* live0;
   uint32_t* live1;
-  uint32_t* fr0;
-  uint32_t* fr1;
-  uint64_t* fa0;
-  uint64_t* fa1;
-  uint32_t* cse0;
-  uint32_t* cse1;
+  Frontier fr[2];
   Acc* acc;  // [3]
   GridBarrier* bar;
-  uint32_t* out;  // kmax, rounds, err
+  uint32_t* out;               // kmax, rounds, err
+  unsigned long long* rtrace;  // [3*4096] per-round expand cycles, Fc, Ftot (diagnostic)
+  unsigned long long* prof;    // [8] block-0 cycles (see dg_kcore_profile)
   int approx;
   uint64_t c_num, c_den;
 };
@@ -68,12 +76,12 @@ struct KcArgs {
 struct Smem {
   uint32_t id[BUF];
   uint32_t dg[BUF];
+  uint64_t of[BUF];
   uint64_t tileA[KC_THREADS];
   uint64_t ws[33];
   uint32_t ws32[33];
   uint32_t cnt;
   unsigned long long baseF, baseL;
-  uint32_t minv;
   // phase scalars fetched by thread 0 after each grid barrier
   uint32_t abort;
   unsigned long long b_front, b_live;
@@ -87,28 +95,25 @@ __device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
   s.b_ovf = ld_relaxed_u32(&acc->ovf);
 }
 
-__device__ __forceinline__ uint32_t deg_full(const uint64_t* offs, uint32_t v) {
-  return uint32_t(offs[v + 1] - offs[v]);
-}
-
-// All threads of the CTA call this with a per-thread candidate (isF, v, d).
-// Publishes the tile's entries into frontier (fr, fa) with one atomic,
-// labels them, and fills the chunk-start table for the tile's arc range.
-__device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d, uint32_t label,
-                                                const KcArgs& a, uint32_t* fr, uint64_t* fa,
-                                                uint32_t* cse, Acc* acc, Smem& s) {
-  uint64_t pk = isF ? ((1ULL << 36) | d) : 0ULL;
+// All threads of the CTA call this with a per-thread candidate (isF, v, d, o).
+// Publishes the tile's entries into the frontier with one atomic, labels
+// them, and fills the chunk-start table for the tile's arc range.
+__device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d, uint64_t o,
+                                                uint32_t label, const KcArgs& a,
+                                                const Frontier& F, Acc* acc, Smem& s) {
+  const uint64_t pk = isF ? ((1ULL << 36) | d) : 0ULL;
   uint64_t tot;
-  uint64_t ex = block_excl_scan(pk, s.ws, &tot);
+  const uint64_t ex = block_excl_scan(pk, s.ws, &tot);
   if (tot == 0) return;  // uniform: nothing in this tile (block_excl_scan synced)
   if (threadIdx.x == 0) s.baseF = atomicAdd(&acc->front, (unsigned long long)tot);
   __syncthreads();
   const uint64_t base = s.baseF;
   const uint64_t e0 = base >> 36, A0 = base & M36;
   if (isF) {
-    uint64_t k = ex >> 36, A = A0 + (ex & M36);
-    fr[e0 + k] = v;
-    fa[e0 + k] = A;
+    const uint64_t k = ex >> 36, A = A0 + (ex & M36);
+    F.v[e0 + k] = v;
+    F.fa[e0 + k] = A;
+    F.fo[e0 + k] = o;
     a.labels[v] = label;
     s.tileA[k] = A;
   }
@@ -120,13 +125,13 @@ __device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d
       const uint64_t x = c * CH;
       uint64_t lo = 0, hi = cnt - 1;  // largest k with tileA[k] <= x
       while (lo < hi) {
-        uint64_t mid = (lo + hi + 1) >> 1;
+        const uint64_t mid = (lo + hi + 1) >> 1;
         if (s.tileA[mid] <= x)
           lo = mid;
         else
           hi = mid - 1;
       }
-      cse[c] = uint32_t(e0 + lo);
+      F.cse[c] = uint32_t(e0 + lo);
     }
   }
   __syncthreads();
@@ -135,31 +140,38 @@ __device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d
 // Scan the live list: alive vertices with deg <= bound join the frontier,
 // the other alive ones are compacted into live_out.
 __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const uint32_t* live_in,
-                        uint32_t* live_out, uint32_t bound, uint32_t label, uint32_t* fr,
-                        uint64_t* fa, uint32_t* cse, Acc* acc, Smem& s) {
+                        uint32_t* live_out, uint32_t bound, uint32_t label, const Frontier& F,
+                        Acc* acc, Smem& s) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < livec; base += stride) {
     const uint64_t i = base + threadIdx.x;
     uint32_t v = 0, d = 0;
+    uint64_t o = 0;
     bool isF = false, isL = false;
     if (i < livec) {
       v = implicit ? uint32_t(i) : live_in[i];
       if (a.labels[v] == kUnset) {
         if (a.deg[v] <= bound) {
           isF = true;
-          d = deg_full(a.offs, v);
+          o = a.offs[v];
+          d = uint32_t(a.offs[v + 1] - o);
         } else {
           isL = true;
         }
       }
     }
     uint32_t totL;
-    uint32_t exL = block_excl_scan<uint32_t>(isL ? 1u : 0u, s.ws32, &totL);
+    const uint32_t exL = block_excl_scan<uint32_t>(isL ? 1u : 0u, s.ws32, &totL);
     if (threadIdx.x == 0 && totL) s.baseL = atomicAdd(&acc->live, (unsigned long long)totL);
     __syncthreads();
     if (isL) live_out[s.baseL + exL] = v;
-    emit_front_tile(isF, v, d, label, a, fr, fa, cse, acc, s);
+    emit_front_tile(isF, v, d, o, label, a, F, acc, s);
   }
+}
+
+// 64-bit warp shuffle
+__device__ __forceinline__ uint64_t shfl64(uint64_t x, uint32_t src) {
+  return __shfl_sync(~0u, x, src);
 }
 
 __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
@@ -180,10 +192,19 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
   uint32_t Fc = 0;
   uint64_t Ftot = 0;
   uint64_t guard = 0;
+  const bool P = blockIdx.x == 0 && threadIdx.x == 0;
+  long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp = clock64();
+  auto mark = [&](int k) {
+    if (P) {
+      const long long tt = clock64();
+      pr[k] += tt - tp;
+      tp = tt;
+    }
+  };
 
   for (;;) {
     if (++guard > 4ULL * a.n + 64) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.out[2] = 1;
+      if (P) a.out[2] = 1;
       break;
     }
     if (Fc == 0) {
@@ -194,21 +215,24 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       uint32_t lmin = kUnset;
       for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < livec;
            i += uint64_t(gridDim.x) * blockDim.x) {
-        uint32_t v = implicit ? uint32_t(i) : live_in[i];
+        const uint32_t v = implicit ? uint32_t(i) : live_in[i];
         if (a.labels[v] == kUnset) lmin = min(lmin, a.deg[v]);
       }
-      lmin = warp_min(lmin);
+      lmin = __reduce_min_sync(~0u, lmin);
       if (lane == 0) s.ws32[threadIdx.x >> 5] = lmin;
       __syncthreads();
       if (threadIdx.x < 32) {
         uint32_t x = threadIdx.x < (blockDim.x >> 5) ? s.ws32[threadIdx.x] : kUnset;
-        x = warp_min(x);
+        x = __reduce_min_sync(~0u, x);
         if (threadIdx.x == 0 && x != kUnset) atomicMin(&acc->minv, x);
       }
+      mark(0);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
+      mark(1);
+      if (P) ++pr[6];
       const uint64_t gmin = s.b_minv;
       if (gmin == kUnset) {  // remaining > 0 but nothing alive: inconsistent
-        if (blockIdx.x == 0 && threadIdx.x == 0) a.out[2] = 2;
+        if (P) a.out[2] = 2;
         break;
       }
       while (gmin > bound) {
@@ -217,18 +241,17 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           label = gmin;
         } else {  // core.cpp:105-110
           label = t;
-          uint64_t ct = (t * a.c_num) / a.c_den + ((t * a.c_num) % a.c_den != 0);
-          uint64_t nt = t + 1 > ct ? t + 1 : ct;
+          const uint64_t ct = (t * a.c_num) / a.c_den + ((t * a.c_num) % a.c_den != 0);
+          const uint64_t nt = t + 1 > ct ? t + 1 : ct;
           bound = nt - 1;
           t = nt;
         }
       }
-      uint32_t* fr = (f & 1) ? a.fr1 : a.fr0;
-      uint64_t* fa = (f & 1) ? a.fa1 : a.fa0;
-      uint32_t* cse = (f & 1) ? a.cse1 : a.cse0;
       collect(a, livec, implicit, live_in, lv ? a.live0 : a.live1, uint32_t(bound),
-              uint32_t(label), fr, fa, cse, acc, s);
+              uint32_t(label), a.fr[f & 1], acc, s);
+      mark(2);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
+      mark(1);
       const unsigned long long pk = s.b_front;
       Fc = uint32_t(pk >> 36);
       Ftot = pk & M36;
@@ -236,7 +259,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       lv ^= 1;
       implicit = false;
       if (Fc == 0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) a.out[2] = 3;
+        if (P) a.out[2] = 3;
         break;
       }
     }
@@ -246,7 +269,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     if (label > kmax) kmax = uint32_t(label);
     remaining -= Fc;
     Acc* nacc = a.acc + ((f + 1) % 3);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (P) {
       Acc* r = a.acc + ((f + 2) % 3);
       r->front = 0;
       r->live = 0;
@@ -256,44 +279,77 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     if (threadIdx.x == 0) s.cnt = 0;
     __syncthreads();
     {
-      const uint32_t* F = (f & 1) ? a.fr1 : a.fr0;
-      const uint64_t* FA = (f & 1) ? a.fa1 : a.fa0;
-      const uint32_t* CS = (f & 1) ? a.cse1 : a.cse0;
+      const Frontier& F = a.fr[f & 1];
       const uint32_t b32 = uint32_t(bound);
-      const uint64_t nchunks = (Ftot + CH - 1) / CH;
-      for (uint64_t c = gwarp; c < nchunks; c += nwarps) {
-        const uint32_t e0 = CS[c];
-        const uint32_t elast = (c + 1 < nchunks) ? CS[c + 1] : Fc - 1;
-        const uint64_t a0 = c * CH;
-        uint32_t us[CH / 32];
+      const uint64_t nch = (Ftot + CH - 1) / CH;
+      for (uint64_t c0 = gwarp; c0 < nch; c0 += nwarps * UC) {
+        // stage UC chunks: entry window [e0, e0 + ne) per chunk, coalesced
+        uint32_t ne[UC];
+        uint64_t e0[UC], fa[UC], fo[UC];
 #pragma unroll
-        for (int j = 0; j < int(CH / 32); ++j) {
-          const uint64_t x = a0 + j * 32 + lane;
-          us[j] = kUnset;
-          if (x < Ftot) {
-            uint32_t lo = e0, hi = elast;
-            while (lo < hi) {  // largest e with FA[e] <= x
-              uint32_t mid = (lo + hi + 1) >> 1;
-              if (FA[mid] <= x)
+        for (int k = 0; k < UC; ++k) {
+          const uint64_t c = c0 + uint64_t(k) * nwarps;
+          ne[k] = 0;
+          e0[k] = 0;
+          fa[k] = ~0ULL;
+          fo[k] = 0;
+          if (c < nch) {
+            e0[k] = F.cse[c];
+            const uint64_t e1 = (c + 1 < nch) ? F.cse[c + 1] : uint64_t(Fc) - 1;
+            ne[k] = uint32_t(e1 - e0[k] + 1);
+            // rows of degree >= 1 need at most 32 entries for 32 arcs; only
+            // zero-degree rows can push the window past 32 (slow path)
+            if (ne[k] > 32 && F.fa[e0[k] + 32] > c * CH + CH - 1) ne[k] = 32;
+            if (lane < ne[k]) {
+              fa[k] = F.fa[e0[k] + lane];
+              fo[k] = F.fo[e0[k] + lane];
+            }
+          }
+        }
+        uint32_t u[UC];
+#pragma unroll
+        for (int k = 0; k < UC; ++k) {
+          const uint64_t c = c0 + uint64_t(k) * nwarps;
+          const uint64_t x = c * CH + lane;
+          u[k] = kUnset;
+          if (c >= nch) continue;  // warp-uniform
+          uint64_t p;
+          if (ne[k] <= 32) {
+            // largest l < ne with fa[l] <= x, by a shuffle search
+            uint32_t l = 0;
+#pragma unroll
+            for (uint32_t step = 16; step; step >>= 1) {
+              const uint32_t tl = l + step;
+              const uint64_t fl = shfl64(fa[k], tl < 32 ? tl : 31);
+              if (tl < ne[k] && fl <= x) l = tl;
+            }
+            p = shfl64(fo[k], l) + (x - shfl64(fa[k], l));
+          } else {  // > 32 entries touch 32 arcs (zero-degree rows): binary search
+            uint64_t lo = e0[k], hi = e0[k] + ne[k] - 1;
+            while (lo < hi) {
+              const uint64_t mid = (lo + hi + 1) >> 1;
+              if (F.fa[mid] <= x)
                 lo = mid;
               else
                 hi = mid - 1;
             }
-            const uint32_t v = F[lo];
-            us[j] = a.adj[a.offs[v] + (x - FA[lo])];
+            p = F.fo[lo] + (x - F.fa[lo]);
           }
+          if (x < Ftot) u[k] = a.adj[p];
         }
 #pragma unroll
-        for (int j = 0; j < int(CH / 32); ++j) {
-          const uint32_t u = us[j];
-          if (u == kUnset) continue;
-          if (a.deg[u] <= b32) continue;  // dead, or already at/below the bound
-          const uint32_t old = atomicSub(&a.deg[u], 1u);
+        for (int k = 0; k < UC; ++k) {
+          const uint32_t uv = u[k];
+          if (uv == kUnset) continue;
+          if (a.deg[uv] <= b32) continue;  // dead, or already at/below the bound
+          const uint32_t old = atomicSub(&a.deg[uv], 1u);
           if (old == b32 + 1) {  // crossed: joins the next round
             const uint32_t slot = atomicAdd(&s.cnt, 1u);
             if (slot < BUF) {
-              s.id[slot] = u;
-              s.dg[slot] = deg_full(a.offs, u);
+              const uint64_t o0 = a.offs[uv];
+              s.id[slot] = uv;
+              s.of[slot] = o0;
+              s.dg[slot] = uint32_t(a.offs[uv + 1] - o0);
             } else {
               nacc->ovf = 1;  // left unlabelled; the overflow collect finds it
             }
@@ -302,26 +358,30 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       }
     }
     __syncthreads();
+    if (P && a.rtrace && rounds <= 4096) {
+      a.rtrace[3 * (rounds - 1)] = clock64() - tp;
+      a.rtrace[3 * (rounds - 1) + 1] = Fc;
+      a.rtrace[3 * (rounds - 1) + 2] = Ftot;
+    }
+    mark(3);
     {
       const uint32_t cnt = min(s.cnt, BUF);
-      uint32_t* fr = ((f + 1) & 1) ? a.fr1 : a.fr0;
-      uint64_t* fa = ((f + 1) & 1) ? a.fa1 : a.fa0;
-      uint32_t* cse = ((f + 1) & 1) ? a.cse1 : a.cse0;
+      const Frontier& NF = a.fr[(f + 1) & 1];
       for (uint32_t b0 = 0; b0 < cnt; b0 += blockDim.x) {
         const uint32_t i = b0 + threadIdx.x;
         const bool ok = i < cnt;
-        emit_front_tile(ok, ok ? s.id[i] : 0, ok ? s.dg[i] : 0, uint32_t(label), a, fr, fa, cse,
-                        nacc, s);
+        emit_front_tile(ok, ok ? s.id[i] : 0, ok ? s.dg[i] : 0, ok ? s.of[i] : 0,
+                        uint32_t(label), a, NF, nacc, s);
       }
     }
+    mark(4);
     if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, nacc); })) break;
+    mark(5);
     ++f;
     if (s.b_ovf) {
-      uint32_t* fr = (f & 1) ? a.fr1 : a.fr0;
-      uint64_t* fa = (f & 1) ? a.fa1 : a.fa0;
-      uint32_t* cse = (f & 1) ? a.cse1 : a.cse0;
+      if (P) ++pr[7];
       collect(a, livec, implicit, lv ? a.live1 : a.live0, lv ? a.live0 : a.live1, uint32_t(bound),
-              uint32_t(label), fr, fa, cse, nacc, s);
+              uint32_t(label), a.fr[f & 1], nacc, s);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, nacc); })) break;
       livec = uint32_t(s.b_live);
       lv ^= 1;
@@ -331,10 +391,12 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     Fc = uint32_t(pk >> 36);
     Ftot = pk & M36;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (P) {
     a.out[0] = kmax;
     a.out[1] = rounds;
     if (ld_relaxed_u32(&a.bar->abort)) a.out[2] = 4;
+    if (a.prof)
+      for (int k = 0; k < 8; ++k) a.prof[k] = pr[k];
   }
 }
 
@@ -358,6 +420,22 @@ __global__ void k_init_acc(Acc* acc, GridBarrier* bar) {
 
 }  // namespace
 
+unsigned long long* kcore_prof_buffer() {
+  static unsigned long long* buf[64] = {};
+  int d = 0;
+  DG_CUDA(cudaGetDevice(&d));
+  if (!buf[d]) {
+    DG_CUDA(cudaMalloc(&buf[d], (8 + 3 * 4096) * sizeof(unsigned long long)));
+    DG_CUDA(cudaMemset(buf[d], 0, (8 + 3 * 4096) * sizeof(unsigned long long)));
+  }
+  return buf[d];
+}
+
+void kcore_profile(unsigned long long out[8 + 3 * 4096]) {
+  d2h(out, kcore_prof_buffer(), 8 + 3 * 4096);
+  stream_sync();
+}
+
 CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
                  uint32_t* d_labels) {
   if (g.n == 0) throw DgError(DG_E_EMPTY, "coreness of empty graph");
@@ -366,8 +444,8 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   if (g.n >= (1ULL << 28) || 2 * g.m >= (1ULL << 36))
     throw DgError(DG_E_PARAM, "graph too large for the single-GPU coreness kernel");
   const uint64_t n = g.n;
-  DevBuf<uint32_t> deg(n), live0(n), live1(n), fr0(n), fr1(n);
-  DevBuf<uint64_t> fa0(n), fa1(n);
+  DevBuf<uint32_t> deg(n), live0(n), live1(n), v0(n), v1(n);
+  DevBuf<uint64_t> fa0(n), fa1(n), fo0(n), fo1(n);
   const uint64_t nch = (2 * g.m) / CH + 2;
   DevBuf<uint32_t> cse0(nch), cse1(nch);
   DevBuf<Acc> acc(3);
@@ -380,20 +458,30 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   DG_CHECK_LAUNCH();
 
   const size_t smem = sizeof(Smem);
-  static bool attr_set = false;
-  if (!attr_set) {
-    DG_CUDA(cudaFuncSetAttribute(k_coreness, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    attr_set = true;
-  }
+  DG_CUDA(cudaFuncSetAttribute(k_coreness, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
   int occ = 0;
   DG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coreness, KC_THREADS, smem));
   if (occ < 1) throw DgError(DG_E_CUDA, "coreness kernel does not fit on an SM");
-  const unsigned blocks = unsigned(num_sms()) * unsigned(occ > 1 ? 1 : occ);
+  const unsigned blocks = unsigned(num_sms());  // one persistent CTA per SM
 
-  KcArgs args{g.offs.get(), g.adj.get(), uint32_t(n), deg.get(), d_labels, live0.get(),
-              live1.get(), fr0.get(), fr1.get(), fa0.get(), fa1.get(), cse0.get(), cse1.get(),
-              acc.get(), bar.get(), out.get(), approx ? 1 : 0, c_num, c_den};
+  KcArgs args{g.offs.get(),
+              g.adj.get(),
+              uint32_t(n),
+              deg.get(),
+              d_labels,
+              live0.get(),
+              live1.get(),
+              {Frontier{v0.get(), fa0.get(), fo0.get(), cse0.get()},
+               Frontier{v1.get(), fa1.get(), fo1.get(), cse1.get()}},
+              acc.get(),
+              bar.get(),
+              out.get(),
+              kcore_prof_buffer() + 8,
+              kcore_prof_buffer(),
+              approx ? 1 : 0,
+              c_num,
+              c_den};
   void* params[] = {&args};
   cudaEvent_t e0, e1;
   DG_CUDA(cudaEventCreate(&e0));
@@ -401,6 +489,7 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   DG_CUDA(cudaEventRecord(e0, stream()));
   DG_CUDA(cudaLaunchCooperativeKernel((void*)k_coreness, dim3(blocks), dim3(KC_THREADS), params,
                                       smem, stream()));
+  count_launch();
   DG_CUDA(cudaEventRecord(e1, stream()));
   uint32_t h[3];
   d2h(h, out.get(), 3);

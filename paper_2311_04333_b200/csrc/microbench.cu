@@ -129,3 +129,14 @@ extern "C" dg_status dg_peel_profile(uint64_t out[16]) {
     return e.code;
   }
 }
+
+extern "C" dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]) {
+  try {
+    static unsigned long long o[8 + 3 * 4096];
+    kcore_profile(o);
+    for (int i = 0; i < 8 + 3 * 4096; ++i) out[i] = o[i];
+    return DG_OK;
+  } catch (const DgError& e) {
+    return e.code;
+  }
+}

@@ -1,0 +1,35 @@
+"""k-core phase split: python tools/kcore_probe.py [scale]"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2311_04333_b200 as dg  # noqa: E402
+
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
+u, v = dg.gen_rmat(scale, 16 << scale, scale)
+g = dg.Graph.from_pairs(u, v)
+del u, v
+for _ in range(2):
+    r = dg.run(g, dg.RunConfig(iterations=1))
+p = np.zeros(8 + 3 * 4096, np.uint64)
+dg.LIB.dg_kcore_profile(p.ctypes.data_as(C.POINTER(C.c_uint64)))
+ghz = 1.965e3
+names = ["lvl_min", "lvl_sync", "collect", "expand", "flush", "exp_sync"]
+print(f"n={g.n} m={g.m} rounds={r.trace.init.peel_rounds} kmax={r.trace.init.kmax} "
+      f"kernel_ms={r.trace.init.coreness_kernel_ms:.3f} levels={p[6]} ovf_collects={p[7]}")
+print("  " + " ".join(f"{k}={p[i] / ghz / 1e3:.3f}ms" for i, k in enumerate(names)))
+
+R = int(r.trace.init.peel_rounds)
+tr = p[8:8 + 3 * min(R, 4096)].reshape(-1, 3).astype(np.int64)
+cyc, fc, ftot = tr[:, 0], tr[:, 1], tr[:, 2]
+order = np.argsort(-cyc)
+print(f"  per-round expand: mean {cyc.mean()/ghz:.2f}us median {np.median(cyc)/ghz:.2f}us; "
+      f"top-20 rounds hold {100*cyc[order[:20]].sum()/cyc.sum():.1f}% of expand time")
+for i in order[:8]:
+    print(f"    round {i+1}: {cyc[i]/ghz:.1f}us Fc={fc[i]} arcs={ftot[i]}")
+small = ftot < 4096
+print(f"  rounds with < 4096 arcs: {small.sum()} taking {cyc[small].sum()/ghz/1e3:.2f}ms "
+      f"({cyc[small].mean()/ghz:.2f}us each); others {(~small).sum()} taking {cyc[~small].sum()/ghz/1e3:.2f}ms")
