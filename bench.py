@@ -51,6 +51,15 @@ CONFIGS = {
 }
 
 
+def traffic():
+    """DRAM bytes per launch of the hot kernels from the committed ncu captures."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -293,9 +302,13 @@ def run_ours(args, cfg, rank, world, local):
                   "kmax": res[0].trace.init.kmax,
                   "roofline": {"bound": "hbm", "achieved": kc_achieved, "peak": hbm,
                                "unit": "GB/s", "frac": kc_achieved / hbm,
-                               "algorithmic_bytes": kc_bytes, "peak_kind": peak_kind}},
+                               "algorithmic_bytes": kc_bytes, "peak_kind": peak_kind,
+                               "traffic": traffic().get("k_coreness", {}).get(
+                                   "dram_bytes_per_launch")}},
         "roofline": {"bound": "hbm", "achieved": peel_achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": peel_achieved / hbm, "traffic": None,
+                     "frac": peel_achieved / hbm,
+                     "traffic": traffic().get("k_peel", {}).get("dram_bytes_per_launch"),
+                     "traffic_note": traffic().get("k_peel", {}).get("launch"),
                      "kernel": "k_peel (Greedy++ batch peel, fused Alg.3 charges)",
                      "bytes_per_launch": "8(n+1) offs + 8m adj + 8n loads + 4n perm + 4n charges",
                      "peak_kind": peak_kind},
