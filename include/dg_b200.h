@@ -212,6 +212,10 @@ dg_status dg_peel_profile(uint64_t out[16]);
  * scans, level-advance barriers, collects, expansion, flushes, expansion
  * barriers; #level advances; #overflow collects. */
 dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]);  /* + per-round trace */
+/* Tuning / testing knob for the Greedy++ ordering kernel: 0 automatic (one CTA
+ * when the core's keys fit one SM, else a thread-block cluster), 1 single CTA
+ * only, 2 cluster whenever it fits.  Results are identical in every mode. */
+dg_status dg_set_peel_mode(int mode);
 
 #ifdef __cplusplus
 }

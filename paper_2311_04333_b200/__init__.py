@@ -489,6 +489,11 @@ def set_device(device: int) -> None:
     _chk(LIB.dg_set_device(device))
 
 
+def set_peel_mode(mode: int) -> None:
+    """0 automatic, 1 single-CTA peel only, 2 cluster peel whenever it fits (testing/tuning)."""
+    _chk(LIB.dg_set_peel_mode(mode))
+
+
 def launch_count() -> int:
     """Kernels of this library launched so far in this process."""
     return LIB.dg_launch_count()

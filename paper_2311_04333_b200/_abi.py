@@ -87,6 +87,7 @@ PROTOTYPES = {
     "dg_microbench": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_double)]),
     "dg_peel_profile": (C.c_int, [u64p]),
     "dg_kcore_profile": (C.c_int, [u64p]),
+    "dg_set_peel_mode": (C.c_int, [C.c_int]),
 }
 
 

@@ -27,6 +27,11 @@ __global__ void __cluster_dims__(8, 1, 1) k_mb_cluster(uint64_t iters) {
   for (uint64_t i = 0; i < iters; ++i) c.sync();
 }
 
+__global__ void k_mb_cluster_dyn(uint64_t iters) {  // cluster size from the launch
+  cg::cluster_group c = cg::this_cluster();
+  for (uint64_t i = 0; i < iters; ++i) c.sync();
+}
+
 __global__ void k_mb_bar(uint64_t iters, uint32_t* sink) {
   uint32_t x = threadIdx.x;
   for (uint64_t i = 0; i < iters; ++i) {
@@ -97,6 +102,23 @@ extern "C" dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op)
       k_mb_chase<<<1, 1, 0, stream()>>>(next.get(), which == 4 ? 1000 : n / 4, sink.get());
       DG_CUDA(cudaEventRecord(e0, stream()));
       k_mb_chase<<<1, 1, 0, stream()>>>(next.get(), iters, sink.get());
+    } else if (which == 9 || which == 10) {  // 16- / 4-CTA cluster barrier, 1024 threads
+      const int cs = which == 9 ? 16 : 4;
+      if (cs > 8)
+        DG_CUDA(cudaFuncSetAttribute(k_mb_cluster_dyn,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(1024);
+      cfg.stream = stream();
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      DG_CUDA(cudaLaunchKernelEx(&cfg, k_mb_cluster_dyn, iters));
     } else if (which == 5 || which == 6) {
       k_mb_atoms<<<1, 1024, 0, stream()>>>(iters, sink.get(), which == 6);
     } else {
@@ -139,4 +161,13 @@ extern "C" dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]) {
   } catch (const DgError& e) {
     return e.code;
   }
+}
+
+namespace dgb {
+extern int g_peel_mode;
+}
+extern "C" dg_status dg_set_peel_mode(int mode) {
+  if (mode < 0 || mode > 2) return DG_E_PARAM;
+  dgb::g_peel_mode = mode;
+  return DG_OK;
 }

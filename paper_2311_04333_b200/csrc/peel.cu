@@ -18,6 +18,7 @@
 
 #include "internal.cuh"
 #include "peel_kernel.cuh"
+#include "peel_cluster.cuh"
 
 namespace dgb {
 
@@ -25,6 +26,12 @@ namespace {
 
 constexpr int PT = 1024;  // peel CTA size
 constexpr size_t kSmemCap = 227 * 1024;
+
+}  // namespace
+
+int g_peel_mode = 0;  // 0 auto, 1 single-CTA only, 2 cluster whenever it fits (dg_set_peel_mode)
+
+namespace {
 
 // ---- key range: min load, max (load - min + deg)
 __global__ void k_key_range(const uint64_t* offs, const uint64_t* loads, uint64_t n,
@@ -291,6 +298,54 @@ KeyRange key_range(const dg_graph& g, const uint64_t* d_loads) {
   return kr;
 }
 
+// Cluster variant: returns false when no cluster configuration fits.
+template <int CS>
+bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
+                    uint32_t* d_perm, uint64_t* d_raw, unsigned long long* d_batches) {
+  const uint64_t n = g.n;
+  uint32_t sh = 10;  // NC = 2^sh >= PT ids per CTA
+  while ((uint64_t(CS) << sh) < n) ++sh;
+  const bool offs32 = 2 * g.m < 0xffffffffULL;
+  bool offs_smem = offs32 && peelc::smem_bytes(sh, true) <= kSmemCap;
+  if (!offs_smem && peelc::smem_bytes(sh, false) > kSmemCap) return false;
+  const size_t smem = peelc::smem_bytes(sh, offs_smem);
+  auto kern = peelc::k_peel_cluster<CS>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (CS > 8 &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS);
+  cfg.blockDim = dim3(peelc::PT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream();
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  peelc::Args a{g.offs.get(), g.adj.get(), uint32_t(n), d_loads, base, one ? 1 : 0,
+                sh, (1u << sh) / peelc::PT, offs_smem ? 1 : 0, d_perm, d_raw, d_batches,
+                peel_prof_buffer()};
+  DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  count_launch();
+  return true;
+}
+
 void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
                 bool one_at_a_time, uint32_t* d_perm, uint64_t* d_raw,
                 unsigned long long* d_batches) {
@@ -309,6 +364,16 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
   const uint32_t chunk_odd = per | 1u;
   const bool offs32 = 2 * g.m < 0xffffffffULL;
   const uint64_t base = kr.min_load;
+  // Cores whose u32 keys + offsets do not fit one SM: a 16- (or 8-) CTA cluster
+  // with the keys spread over distributed shared memory.
+  // Preference: one CTA with u32 keys in shared memory (fastest per batch);
+  // when the core's keys do not fit one SM, a 16- (or 8-) CTA cluster with the
+  // keys spread over distributed shared memory; then the u64 / global-key
+  // single-CTA fallbacks.  dg_set_peel_mode can force either kernel.
+  if (k32 && g_peel_mode == 2) {
+    if (launch_cluster<16>(g, d_loads, base, one_at_a_time, d_perm, d_raw, d_batches)) return;
+    if (launch_cluster<8>(g, d_loads, base, one_at_a_time, d_perm, d_raw, d_batches)) return;
+  }
   if (k32) {
     if (offs32 && peelk::smem_bytes<uint32_t, true>(4 * vq, true) <= kSmemCap &&
         launch_vec<true>(g, d_loads, base, one_at_a_time, vq, d_perm, d_raw, d_batches))
@@ -316,6 +381,10 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
     if (peelk::smem_bytes<uint32_t, false>(4 * vq, true) <= kSmemCap &&
         launch_vec<false>(g, d_loads, base, one_at_a_time, vq, d_perm, d_raw, d_batches))
       return;
+    if (g_peel_mode != 1) {
+      if (launch_cluster<16>(g, d_loads, base, one_at_a_time, d_perm, d_raw, d_batches)) return;
+      if (launch_cluster<8>(g, d_loads, base, one_at_a_time, d_perm, d_raw, d_batches)) return;
+    }
   }
 #define DG_PEEL_TRY(K, SM, OF)                                                               \
   if ((sizeof(K) == 4) == k32 && (!OF || offs32) &&                                          \

@@ -312,3 +312,37 @@ def test_cpp_dropin_api_on_device():
     subprocess.run(cmd, check=True)
     r = subprocess.run([out], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_peel_kernel_modes_agree(dg, orc, golden, mode):
+    """The single-CTA (mode 1) and the thread-block-cluster (mode 2) Greedy++
+    kernels must both reproduce the reference bit for bit."""
+    dg.set_peel_mode(mode)
+    try:
+        for c in golden["peel"][::3]:
+            g = dg.Graph.from_pairs(*orc.gen_gnp(c["n"], c["permille"], c["seed"]))
+            loads = random_loads(g.n, c["loads_maxload"], c["loads_seed"])
+            assert dg.load_peel_order(g, loads).perm.tolist() == c["perm"]
+            assert dg.load_peel_order(g, loads, True).perm.tolist() == c["perm_one"]
+        u, v = dg.gen_rmat(15, 16 << 15, 23)
+        g = dg.Graph.from_pairs(u, v)
+        h = orc.build(u, v)
+        d = dg.exact_coreness(g)
+        core = dg.get_core(g, d, (d.kmax + 1) // 2)
+        lab, kmax, _ = orc.coreness(h)
+        hc, _ = orc.get_core(h, lab, (kmax + 1) // 2)
+        ld, lh = np.zeros(core.n, np.uint64), np.zeros(core.n, np.uint64)
+        for _ in range(4):
+            p = dg.load_peel_order(core, ld).perm
+            assert np.array_equal(p, orc.peel_order(hc, lh))
+            dg.density_and_load_update(core, p, ld)
+            _, lh, _, _ = orc.density_update(hc, p, lh)
+            assert np.array_equal(ld, lh)
+        r = dg.run(g, dg.RunConfig(iterations=6))
+        o = orc.run(h, ORunConfig(iterations=6))
+        assert (r.best.edges, r.best.verts) == o.best and np.array_equal(r.witness, o.witness)
+        assert [(t.iter, t.rho.edges, t.rho.verts, t.n, t.m, t.width)
+                for t in r.trace.iters] == o.trace
+    finally:
+        dg.set_peel_mode(0)

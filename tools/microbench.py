@@ -9,8 +9,9 @@ import paper_2311_04333_b200 as dg  # noqa: E402
 
 NAMES = ["grid_barrier_ns", "cg_grid_sync_ns", "cluster8_sync_ns", "cta_syncthreads_ns",
          "dependent_load_4MiB_ns", "smem_atomic_per_warp_instr_ns",
-         "smem_plain_rmw_per_warp_instr_ns", "dependent_load_64MiB_ns", "dependent_load_1GiB_ns"]
-ITERS = [20000, 20000, 100000, 1000000, 200000, 20000, 20000, 200000, 100000]
+         "smem_plain_rmw_per_warp_instr_ns", "dependent_load_64MiB_ns", "dependent_load_1GiB_ns",
+         "cluster16_sync_ns", "cluster4_sync_ns"]
+ITERS = [20000, 20000, 100000, 1000000, 200000, 20000, 20000, 200000, 100000, 100000, 100000]
 out = {}
 for i, (name, it) in enumerate(zip(NAMES, ITERS)):
     ns = C.c_double()

@@ -30,3 +30,14 @@ print(f"last peel launch: batches={prof[3]} cycles/batch S1={prof[0]/max(1,prof[
       f"(split {100*prof[0]/tot:.0f}/{100*prof[1]/tot:.0f}/{100*prof[2]/tot:.0f}%) "
       f"single-vertex batches={prof[5]} S3/single={prof[4]/max(1,prof[5]):.0f} "
       f"S3/multi={(prof[2]-prof[4])/max(1,prof[3]-prof[5]):.0f} big={prof[6]}")
+if len(sys.argv) > 3:  # also time iteration 1's core with the other kernel mode
+    mode = int(sys.argv[3])
+    dg.set_peel_mode(mode)
+    r = dg.run(g, dg.RunConfig(iterations=2))
+    it = r.trace.iters[0]
+    dg.LIB.dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
+    print(f"mode {mode}: it1 n={it.n} batches={it.batches} order={it.order_ms:.3f}ms "
+          f"us/batch={1e3 * it.order_ms / max(1, it.batches):.2f}")
+    print(f"  last launch (it2) cycles/batch S1={prof[0]/max(1,prof[3]):.0f} "
+          f"S2={prof[1]/max(1,prof[3]):.0f} S3={prof[2]/max(1,prof[3]):.0f} CS={prof[7]}")
+    dg.set_peel_mode(0)
