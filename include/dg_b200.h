@@ -176,6 +176,30 @@ dg_status dg_run(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res
                  dg_iter_record* trace, uint64_t trace_cap, uint64_t* witness,
                  uint64_t witness_cap, uint64_t* final_ids, uint64_t final_cap);
 
+/* ------------------------------------------------------------ sharded coreness */
+
+/* One GPU's shard of a 1D vertex-range-partitioned exact coreness
+ * (same rounds and labels as exact_coreness, core.cpp:89-119).
+ * Rank `rank` of P owns dense ids [bounds[rank], bounds[rank+1]).  Per round:
+ * dg_shard_count_remote -> exchange counts -> dg_shard_expand (local
+ * decrements + remote ids bucketed by owner into a device send buffer at the
+ * given per-rank displacements) -> all-to-all -> dg_shard_apply (received
+ * decrements) -> all-reduce of the next frontier sizes; when the global
+ * frontier is empty: dg_shard_min_alive -> all-reduce(min) -> dg_shard_collect.
+ * The protocol is paper_2311_04333_b200/sharded.py. */
+typedef struct dg_shard dg_shard;
+dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P, uint32_t rank,
+                          dg_shard** out);
+void dg_shard_free(dg_shard* s);
+dg_status dg_shard_min_alive(dg_shard* s, uint32_t* min_degree);  /* UINT32_MAX if none */
+dg_status dg_shard_collect(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* nfront);
+dg_status dg_shard_count_remote(dg_shard* s, uint64_t* counts /* P entries */);
+dg_status dg_shard_expand(dg_shard* s, uint32_t bound, uint32_t label, const uint64_t* displs,
+                          uint32_t* d_send /* device */);
+dg_status dg_shard_apply(dg_shard* s, const uint32_t* d_recv /* device */, uint64_t nrecv,
+                         uint32_t bound, uint32_t label, uint64_t* nnext);
+dg_status dg_shard_labels(const dg_shard* s, uint32_t* labels /* hi - lo entries */);
+
 /* ------------------------------------------------------------ synthetic inputs */
 
 /* Seeded counter-based generators (bit-identical to oracle/dg_oracle.c).

@@ -73,6 +73,14 @@ PROTOTYPES = {
     "dg_run": (C.c_int, [GP, C.POINTER(DgRunConfig), C.POINTER(DgRunResult),
                          C.POINTER(DgIterRecord), C.c_uint64, u64p, C.c_uint64, u64p,
                          C.c_uint64]),
+    "dg_shard_create": (C.c_int, [GP, u64p, C.c_uint32, C.c_uint32, GPP]),
+    "dg_shard_free": (None, [GP]),
+    "dg_shard_min_alive": (C.c_int, [GP, u32p]),
+    "dg_shard_collect": (C.c_int, [GP, C.c_uint32, C.c_uint32, u64p]),
+    "dg_shard_count_remote": (C.c_int, [GP, u64p]),
+    "dg_shard_expand": (C.c_int, [GP, C.c_uint32, C.c_uint32, u64p, C.c_void_p]),
+    "dg_shard_apply": (C.c_int, [GP, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, u64p]),
+    "dg_shard_labels": (C.c_int, [GP, u32p]),
     "dg_gen_rmat": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                               C.c_int]),
     "dg_gen_chung_lu": (C.c_int, [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, C.c_void_p,

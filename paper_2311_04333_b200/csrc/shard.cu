@@ -1,0 +1,248 @@
+// shard.cu -- one GPU's shard of a 1D vertex-range-partitioned coreness
+// (SURVEY.md §8e).  Rank r owns the contiguous dense-id range [lo, hi): its
+// residual degrees and labels; frontier expansion decrements owned
+// neighbours in place (atomicSub crossing detection, as in kcore.cu) and
+// buckets every remote neighbour id by its owner rank for the per-round
+// exchange; received decrements are applied with the same crossing rule.
+// The round / level protocol (frontier-size sum, min-degree agreement,
+// decrement all-to-all) lives in paper_2311_04333_b200/sharded.py over NCCL.
+#include <vector>
+
+#include "internal.cuh"
+
+struct dg_shard {
+  const dg_graph* g = nullptr;  // rows of [lo, hi) are read from this CSR
+  uint64_t lo = 0, hi = 0;
+  dgb::DevBuf<uint32_t> deg, labels, front, next;
+  dgb::DevBuf<unsigned long long> cnt;  // [0] next size, [1] min, [2..] per-rank counts
+  uint64_t nfront = 0;
+  dgb::DevBuf<uint64_t> bounds;  // rank boundaries (P + 1)
+  uint32_t P = 0;
+};
+
+namespace dgb {
+namespace {
+
+constexpr uint32_t kUnset = 0xffffffffu;
+
+__global__ void k_sh_init(const uint64_t* offs, uint64_t lo, uint64_t nl, uint32_t* deg,
+                          uint32_t* labels) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nl;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    deg[i] = uint32_t(offs[lo + i + 1] - offs[lo + i]);
+    labels[i] = kUnset;
+  }
+}
+
+__global__ void k_sh_min(const uint32_t* deg, const uint32_t* labels, uint64_t nl,
+                         unsigned long long* out) {
+  uint32_t m = kUnset;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nl;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    if (labels[i] == kUnset) m = min(m, deg[i]);
+  m = __reduce_min_sync(~0u, m);
+  if (lane_id() == 0 && m != kUnset) atomicMin(out, (unsigned long long)m);
+}
+
+__global__ void k_sh_collect(uint32_t* deg, uint32_t* labels, uint64_t nl, uint32_t bound,
+                             uint32_t label, uint32_t* front, unsigned long long* cnt) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nl;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    if (labels[i] == kUnset && deg[i] <= bound) {
+      labels[i] = label;
+      front[atomicAdd(cnt, 1ULL)] = uint32_t(i);
+    }
+}
+
+__device__ __forceinline__ uint32_t owner_of(const uint64_t* bounds, uint32_t P, uint64_t u) {
+  uint32_t r = 0;
+  while (r + 1 < P && u >= bounds[r + 1]) ++r;
+  return r;
+}
+
+// crossing rule of kcore.cu: the decrement that takes deg from bound+1 to
+// bound enrols the vertex in the next round's frontier
+__device__ __forceinline__ void dec_local(uint32_t* deg, uint32_t* labels, uint32_t i,
+                                          uint32_t bound, uint32_t label, uint32_t* next,
+                                          unsigned long long* cnt) {
+  if (deg[i] <= bound) return;
+  if (atomicSub(&deg[i], 1u) == bound + 1) {
+    labels[i] = label;
+    next[atomicAdd(cnt, 1ULL)] = i;
+  }
+}
+
+// pass 1 (count) / pass 2 (fill + local decrements): warp per frontier vertex
+template <bool FILL>
+__global__ void k_sh_expand(const uint64_t* offs, const uint32_t* adj, uint64_t lo, uint64_t hi,
+                            const uint32_t* front, uint64_t nfront, const uint64_t* bounds,
+                            uint32_t P, uint32_t* deg, uint32_t* labels, uint32_t bound,
+                            uint32_t label, uint32_t* next, unsigned long long* cnt,
+                            unsigned long long* cursor, uint32_t* send) {
+  const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t f = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; f < nfront;
+       f += warps) {
+    const uint64_t v = lo + front[f];
+    for (uint64_t p = offs[v] + lane_id(); p < offs[v + 1]; p += 32) {
+      const uint64_t u = adj[p];
+      if (u >= lo && u < hi) {
+        if (FILL) dec_local(deg, labels, uint32_t(u - lo), bound, label, next, cnt);
+      } else {
+        const uint32_t r = owner_of(bounds, P, u);
+        if (FILL)
+          send[atomicAdd(&cursor[r], 1ULL)] = uint32_t(u);
+        else
+          atomicAdd(&cnt[2 + r], 1ULL);
+      }
+    }
+  }
+}
+
+__global__ void k_sh_apply(const uint32_t* recv, uint64_t nrecv, uint64_t lo, uint32_t* deg,
+                           uint32_t* labels, uint32_t bound, uint32_t label, uint32_t* next,
+                           unsigned long long* cnt) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nrecv;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    dec_local(deg, labels, uint32_t(recv[i] - lo), bound, label, next, cnt);
+}
+
+}  // namespace
+}  // namespace dgb
+
+using namespace dgb;
+
+#define SH_TRY try {
+#define SH_END                  \
+  return DG_OK;                 \
+  }                             \
+  catch (const DgError& e) {    \
+    return e.code;              \
+  }                             \
+  catch (...) {                 \
+    return DG_E_INVARIANT;      \
+  }
+
+extern "C" {
+
+dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P, uint32_t rank,
+                          dg_shard** out) {
+  SH_TRY
+  if (!g || !bounds || !out || rank >= P) throw DgError(DG_E_PARAM, "bad shard arguments");
+  auto s = std::make_unique<dg_shard>();
+  s->g = g;
+  s->P = P;
+  s->lo = bounds[rank];
+  s->hi = bounds[rank + 1];
+  if (s->lo > s->hi || s->hi > g->n) throw DgError(DG_E_PARAM, "bad shard range");
+  const uint64_t nl = s->hi - s->lo;
+  s->deg.alloc(nl);
+  s->labels.alloc(nl);
+  s->front.alloc(nl);
+  s->next.alloc(nl);
+  s->cnt.alloc(2 + P);
+  s->bounds.alloc(P + 1);
+  h2d(s->bounds.get(), bounds, P + 1);
+  if (nl) {
+    k_sh_init<<<grid_for(nl, 256), 256, 0, stream()>>>(g->offs.get(), s->lo, nl, s->deg.get(),
+                                                        s->labels.get());
+    DG_CHECK_LAUNCH();
+  }
+  stream_sync();
+  *out = s.release();
+  SH_END
+}
+
+void dg_shard_free(dg_shard* s) {
+  try {
+    delete s;
+  } catch (...) {
+  }
+}
+
+dg_status dg_shard_min_alive(dg_shard* s, uint32_t* out) {
+  SH_TRY
+  const uint64_t nl = s->hi - s->lo;
+  unsigned long long init = kUnset;
+  h2d(s->cnt.get() + 1, &init, 1);
+  if (nl) {
+    k_sh_min<<<grid_for(nl, 256), 256, 0, stream()>>>(s->deg.get(), s->labels.get(), nl,
+                                                       s->cnt.get() + 1);
+    DG_CHECK_LAUNCH();
+  }
+  *out = uint32_t(read_scalar(s->cnt.get() + 1));
+  SH_END
+}
+
+dg_status dg_shard_collect(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* nfront) {
+  SH_TRY
+  const uint64_t nl = s->hi - s->lo;
+  s->cnt.zero();
+  if (nl) {
+    k_sh_collect<<<grid_for(nl, 256), 256, 0, stream()>>>(s->deg.get(), s->labels.get(), nl,
+                                                           bound, label, s->front.get(),
+                                                           s->cnt.get());
+    DG_CHECK_LAUNCH();
+  }
+  s->nfront = read_scalar(s->cnt.get());
+  *nfront = s->nfront;
+  SH_END
+}
+
+dg_status dg_shard_count_remote(dg_shard* s, uint64_t* counts) {
+  SH_TRY
+  s->cnt.zero();
+  if (s->nfront) {
+    k_sh_expand<false><<<grid_for(s->nfront * 32, 256), 256, 0, stream()>>>(
+        s->g->offs.get(), s->g->adj.get(), s->lo, s->hi, s->front.get(), s->nfront,
+        s->bounds.get(), s->P, s->deg.get(), s->labels.get(), 0, 0, nullptr, s->cnt.get(),
+        nullptr, nullptr);
+    DG_CHECK_LAUNCH();
+  }
+  std::vector<unsigned long long> h(s->P);
+  d2h(h.data(), s->cnt.get() + 2, s->P);
+  stream_sync();
+  for (uint32_t r = 0; r < s->P; ++r) counts[r] = h[r];
+  SH_END
+}
+
+dg_status dg_shard_expand(dg_shard* s, uint32_t bound, uint32_t label, const uint64_t* displs,
+                          uint32_t* d_send) {
+  SH_TRY
+  DevBuf<unsigned long long> cur(s->P);
+  std::vector<unsigned long long> h(displs, displs + s->P);
+  h2d(cur.get(), h.data(), s->P);
+  s->cnt.zero();
+  if (s->nfront) {
+    k_sh_expand<true><<<grid_for(s->nfront * 32, 256), 256, 0, stream()>>>(
+        s->g->offs.get(), s->g->adj.get(), s->lo, s->hi, s->front.get(), s->nfront,
+        s->bounds.get(), s->P, s->deg.get(), s->labels.get(), bound, label, s->next.get(),
+        s->cnt.get(), cur.get(), d_send);
+    DG_CHECK_LAUNCH();
+  }
+  stream_sync();
+  SH_END
+}
+
+dg_status dg_shard_apply(dg_shard* s, const uint32_t* d_recv, uint64_t nrecv, uint32_t bound,
+                         uint32_t label, uint64_t* nnext) {
+  SH_TRY
+  if (nrecv) {
+    k_sh_apply<<<grid_for(nrecv, 256), 256, 0, stream()>>>(d_recv, nrecv, s->lo, s->deg.get(),
+                                                           s->labels.get(), bound, label,
+                                                           s->next.get(), s->cnt.get());
+    DG_CHECK_LAUNCH();
+  }
+  s->nfront = read_scalar(s->cnt.get());
+  std::swap(s->front, s->next);
+  *nnext = s->nfront;
+  SH_END
+}
+
+dg_status dg_shard_labels(const dg_shard* s, uint32_t* labels) {
+  SH_TRY
+  d2h(labels, s->labels.get(), s->hi - s->lo);
+  stream_sync();
+  SH_END
+}
+
+}  // extern "C"

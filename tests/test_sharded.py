@@ -1,0 +1,142 @@
+"""Range-sharded coreness: protocol on CPU (numpy shards,
+in-process and world_size-2 gloo), CUDA shard kernels on the GPU.  Every
+case is checked against the oracle's og_coreness (core.cpp:89-119):
+labels, kmax and peel_rounds bit-exact."""
+import os
+import socket
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+from graphs import biclique_with_k4, clique, path_graph, star, triangle_pendant, uv
+from shard_numpy import NumpyShard
+
+from paper_2311_04333_b200.sharded import LocalComm, TorchComm, partition, sharded_coreness
+
+APPROX = [None, (3, 2), (2, 1)]
+
+
+def _graphs(orc):
+    out = {}
+    for name, e in [("path", path_graph(9)), ("clique", clique(7)), ("star", star(12)),
+                    ("tri_pendant", triangle_pendant()), ("biclique_k4", biclique_with_k4())]:
+        out[name] = orc.build(*uv(e))
+    out["gnp"] = orc.build(*orc.gen_gnp(300, 40, 7))
+    out["rmat10"] = orc.build(*orc.gen_rmat(10, 16 * 1024, 3))
+    out["planted"] = orc.build(*orc.gen_er_planted(2000, 6000, 30, 5))
+    return out
+
+
+def _check(orc, g, labs, kmax, rounds, approx):
+    if approx is None:
+        lab, k, r = orc.coreness(g)
+    else:
+        lab, k, r = orc.coreness(g, True, *approx)
+    np.testing.assert_array_equal(np.concatenate(labs).astype(np.uint32), lab)
+    assert (kmax, rounds) == (k, r)
+
+
+def test_partition_balanced(orc):
+    g = orc.build(*orc.gen_rmat(12, 64 * 1024, 9))
+    for P in (1, 2, 3, 8, 64):
+        b = partition(g.offs, P)
+        assert len(b) == P + 1 and b[0] == 0 and b[-1] == g.n
+        assert np.all(np.diff(b.astype(np.int64)) >= 0)
+        arcs = np.diff(g.offs[b.astype(np.int64)].astype(np.int64))
+        # every range within one max-degree row of the ideal share
+        assert arcs.max() <= int(g.offs[-1]) // P + g.max_degree() + 1
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5])
+def test_protocol_numpy_local(orc, P):
+    for name, g in _graphs(orc).items():
+        for approx in APPROX:
+            b = partition(g.offs, P)
+            shards = [NumpyShard(g.offs, g.adj, b, r) for r in range(P)]
+            labs, kmax, rounds = sharded_coreness(shards, LocalComm(P, "cpu"), g.n, approx)
+            _check(orc, g, labs, kmax, rounds, approx)
+
+
+def test_protocol_rejects_bad_input(orc):
+    g = orc.build(*uv(clique(4)))
+    b = partition(g.offs, 2)
+    shards = [NumpyShard(g.offs, g.adj, b, 0)]  # one of two shards missing
+    with pytest.raises(ValueError):
+        sharded_coreness(shards, LocalComm(2, "cpu"), g.n)
+    with pytest.raises(ValueError):
+        sharded_coreness([NumpyShard(g.offs, g.adj, b, r) for r in range(2)],
+                         LocalComm(2, "cpu"), g.n, (1, 1))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, outdir):
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                     "oracle"))
+    import torch.distributed as dist
+    from oracle import Oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        res = {}
+        for name, g in _graphs(orc).items():
+            for ai, approx in enumerate(APPROX):
+                b = partition(g.offs, world)
+                comm = TorchComm("cpu")
+                labs, kmax, rounds = sharded_coreness([NumpyShard(g.offs, g.adj, b, rank)],
+                                                      comm, g.n, approx)
+                full = np.concatenate(comm.allgather(labs[0]))
+                res[f"{name}/{ai}"] = (full, kmax, rounds)
+        if rank == 0:
+            np.save(os.path.join(outdir, "res.npy"), res, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2(orc):
+    """world_size-2 gloo run of the NCCL protocol (one shard per process)."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gloo_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = np.load(os.path.join(d, "res.npy"), allow_pickle=True).item()
+    gs = _graphs(orc)
+    assert len(res) == len(gs) * len(APPROX)
+    for name, g in gs.items():
+        for ai, approx in enumerate(APPROX):
+            full, kmax, rounds = res[f"{name}/{ai}"]
+            _check(orc, g, [full], kmax, rounds, approx)
+
+
+# ------------------------------------------------------------------ CUDA shard kernels
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 4, 7])
+def test_cuda_shards_local(orc, dg, P):
+    from paper_2311_04333_b200.sharded import coreness_local_shards
+    for name, hg in _graphs(orc).items():
+        g = dg.Graph.from_csr(hg.offs, hg.adj, hg.orig)
+        for approx in APPROX:
+            dec = coreness_local_shards(g, P, approx)
+            _check(orc, hg, [dec.labels], dec.kmax, dec.peel_rounds, approx)
+
+
+@pytest.mark.gpu
+def test_cuda_shards_rmat16(orc, dg):
+    """Larger graph: 8 shards vs the single-GPU kernel and the oracle."""
+    from paper_2311_04333_b200.sharded import coreness_local_shards
+    u, v = orc.gen_rmat(16, 16 << 16, 16)
+    hg = orc.build(u, v)
+    g = dg.Graph.from_csr(hg.offs, hg.adj, hg.orig)
+    dec = coreness_local_shards(g, 8)
+    one = dg.exact_coreness(g)
+    np.testing.assert_array_equal(dec.labels, one.labels)
+    assert (dec.kmax, dec.peel_rounds) == (one.kmax, one.peel_rounds)
+    _check(orc, hg, [dec.labels], dec.kmax, dec.peel_rounds, None)
