@@ -228,10 +228,18 @@ dg_status dg_flush_l2(void);
  * (1024 threads), 4 dependent L2 load, 5 shared atomicAdd per warp
  * instruction (spread addresses), 6 plain shared load+store per warp instr. */
 dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op);
-/* Diagnostic: thread-0 SM cycles of the last Greedy++ peel launch spent in
- * S1 (min scan), S2 (batch extraction), S3 (removal), its batch count, S3
- * cycles of single-vertex batches, their count, #batches > 32, n. */
+/* Diagnostic (instrumented launches only, see dg_peel_trace_arm): thread-0 SM
+ * cycles of the last Greedy++ peel launch spent in S1 (min scan), S2 (batch
+ * extraction), S3 (removal), its batch count, S3 cycles of single-vertex
+ * batches, their count, #batches > 32, n, #batches on the table path. */
 dg_status dg_peel_profile(uint64_t out[16]);
+/* Diagnostic: launch the instrumented single-CTA peel (fills dg_peel_profile)
+ * and record a per-warp timeline (SM cycles) of batches [first_batch,
+ * first_batch + 8) of subsequent launches; 0xFFFFFFFF disarms.  Read it as
+ * [8 batches][32 warps][12 stamps]: loop top, S1 done, S2 start, S2 done,
+ * S3 start, S3 done, then adjacency-load latency probes. */
+dg_status dg_peel_trace_arm(uint32_t first_batch);
+dg_status dg_peel_trace_read(uint64_t out[8 * 32 * 12]);
 /* Diagnostic: block-0 cycles of the last coreness launch in level-advance min
  * scans, level-advance barriers, collects, expansion, flushes, expansion
  * barriers; #level advances; #overflow collects. */

@@ -94,6 +94,8 @@ PROTOTYPES = {
     "dg_flush_l2": (C.c_int, []),
     "dg_microbench": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_double)]),
     "dg_peel_profile": (C.c_int, [u64p]),
+    "dg_peel_trace_arm": (C.c_int, [C.c_uint32]),
+    "dg_peel_trace_read": (C.c_int, [u64p]),
     "dg_kcore_profile": (C.c_int, [u64p]),
     "dg_set_peel_mode": (C.c_int, [C.c_int]),
 }
@@ -113,4 +115,4 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     return lib
 
 
-LIB = load()
+LIB = load(os.environ.get("DG_B200_LIB", LIB_PATH))

@@ -30,14 +30,14 @@ def _headers():
     return hs + [os.path.join(ROOT, "include", "dg_b200.h")]
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(src: str, verbose: bool, extra=(), obj_dir: str = OBJ) -> str:
+    obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
     newest = max(os.path.getmtime(p) for p in [src] + _headers())
     if os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(OBJ, os.path.basename(src) + ".ptxas.log")
+    log = os.path.join(obj_dir, os.path.basename(src) + ".ptxas.log")
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)
     if r.returncode != 0:
@@ -47,22 +47,30 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = True) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = True, extra=(), tag: str = "") -> str:
+    """Build libdg_b200.so; `extra` nvcc flags + `tag` build a tuning variant
+    libdg_b200_<tag>.so (load it with DG_B200_LIB=<path>)."""
+    obj_dir = OBJ + (f"_{tag}" if tag else "")
+    lib = LIB if not tag else os.path.join(PKG, f"libdg_b200_{tag}.so")
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl",
+        objs = list(ex.map(lambda s: _compile(s, verbose, extra, obj_dir), srcs))
+    if not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl",
                "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
         if verbose:
-            print(f"[build] linked {LIB}", flush=True)
-    return LIB
+            print(f"[build] linked {lib}", flush=True)
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose=True)
+    # python build.py [tag -DFLAG ...]
+    if len(sys.argv) > 1:
+        build(verbose=True, extra=sys.argv[2:], tag=sys.argv[1])
+    else:
+        build(verbose=True)
     sys.exit(0)

@@ -56,6 +56,11 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
 KeyRange key_range(const dg_graph& g, const uint64_t* d_loads);
 // thread-0 cycle split (S1, S2, S3, batches) of the last peel launch
 void peel_profile(unsigned long long out[16]);
+// per-warp phase timeline of kPeelTraceBatches batches (dg_peel_trace_*)
+constexpr uint32_t kPeelTraceBatches = 8, kPeelTraceStamps = 12;
+constexpr size_t kPeelTraceWords = size_t(kPeelTraceBatches) * 32 * kPeelTraceStamps;
+void peel_trace_arm(uint32_t first_batch);
+void peel_trace_read(unsigned long long* out);
 void sort_order(uint64_t n, const uint64_t* d_loads, uint32_t* d_perm);
 // A[i] from an arbitrary permutation (refine.cpp:186-199); throws InvariantError
 // on a non-permutation.

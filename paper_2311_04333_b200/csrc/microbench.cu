@@ -1,3 +1,4 @@
+#include <vector>
 // microbench.cu -- latency floors that bound the per-round (k-core) and
 // per-batch (Greedy++) costs on this B200: grid barrier, cooperative-groups
 // grid.sync, cluster barrier, CTA barrier, dependent L2 load chain, shared
@@ -146,6 +147,26 @@ extern "C" dg_status dg_peel_profile(uint64_t out[16]) {
     unsigned long long o[16];
     peel_profile(o);
     for (int i = 0; i < 16; ++i) out[i] = o[i];
+    return DG_OK;
+  } catch (const DgError& e) {
+    return e.code;
+  }
+}
+
+extern "C" dg_status dg_peel_trace_arm(uint32_t first_batch) {
+  try {
+    peel_trace_arm(first_batch);
+    return DG_OK;
+  } catch (const DgError& e) {
+    return e.code;
+  }
+}
+
+extern "C" dg_status dg_peel_trace_read(uint64_t* out) {
+  try {
+    std::vector<unsigned long long> o(kPeelTraceWords);
+    peel_trace_read(o.data());
+    for (size_t i = 0; i < kPeelTraceWords; ++i) out[i] = o[i];
     return DG_OK;
   } catch (const DgError& e) {
     return e.code;

@@ -238,24 +238,38 @@ unsigned long long* peel_prof_buffer() {
   int d = 0;
   DG_CUDA(cudaGetDevice(&d));
   if (!buf[d]) {
-    DG_CUDA(cudaMalloc(&buf[d], 16 * sizeof(unsigned long long)));
-    DG_CUDA(cudaMemset(buf[d], 0, 16 * sizeof(unsigned long long)));
+    constexpr size_t N = 16 + kPeelTraceWords;  // counters, then the armed timeline
+    DG_CUDA(cudaMalloc(&buf[d], N * sizeof(unsigned long long)));
+    DG_CUDA(cudaMemset(buf[d], 0, N * sizeof(unsigned long long)));
   }
   return buf[d];
 }
 
-template <class K, bool SMEM, bool OFFS, int VQ>
+bool g_peel_trace_armed[64] = {};  // dg_peel_trace_arm: launch the timeline variant
+
+bool peel_trace_armed() {
+  int d = 0;
+  DG_CUDA(cudaGetDevice(&d));
+  return g_peel_trace_armed[d];
+}
+
+template <class K, bool SMEM, bool OFFS, int VQ, bool TR = false>
 void launch_peel(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
                  uint32_t chunk, uint32_t* d_perm, uint64_t* d_raw,
                  unsigned long long* d_batches) {
   DevBuf<K> gk;
   if (!SMEM) gk.alloc(size_t(chunk) * peelk::PT);
   const size_t smem = peelk::smem_bytes<K, OFFS>(chunk, SMEM);
-  auto kern = peelk::k_peel<K, SMEM, OFFS, VQ>;
+  auto kern = peelk::k_peel<K, SMEM, OFFS, VQ, TR>;
   DG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   peelk::Args<K> a{g.offs.get(), g.adj.get(), uint32_t(g.n), d_loads, base, one ? 1 : 0,
                    gk.get(), chunk, d_perm, d_raw, d_batches, peel_prof_buffer()};
-  kern<<<1, peelk::PT, smem, stream()>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(peelk::PT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream();
+  DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   DG_CHECK_LAUNCH();
 }
 
@@ -266,8 +280,12 @@ bool launch_vec(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool 
   switch (vq) {
 #define DG_VQ(V)                                                                         \
   case V:                                                                                \
-    launch_peel<uint32_t, true, OFFS, V>(g, d_loads, base, one, 4 * V, d_perm, d_raw,    \
-                                         d_batches);                                     \
+    if (OFFS && peel_trace_armed())                                                      \
+      launch_peel<uint32_t, true, OFFS, V, OFFS>(g, d_loads, base, one, 4 * V, d_perm,   \
+                                                 d_raw, d_batches);                      \
+    else                                                                                 \
+      launch_peel<uint32_t, true, OFFS, V>(g, d_loads, base, one, 4 * V, d_perm, d_raw,  \
+                                           d_batches);                                   \
     return true;
     DG_VQ(1) DG_VQ(3) DG_VQ(5) DG_VQ(7) DG_VQ(9) DG_VQ(11) DG_VQ(13)
 #undef DG_VQ
@@ -405,6 +423,20 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
 
 void peel_profile(unsigned long long out[16]) {
   d2h(out, peel_prof_buffer(), 16);
+  stream_sync();
+}
+
+void peel_trace_arm(uint32_t first_batch) {
+  int d = 0;
+  DG_CUDA(cudaGetDevice(&d));
+  g_peel_trace_armed[d] = first_batch != 0xffffffffu;
+  const unsigned long long w = g_peel_trace_armed[d] ? first_batch + 1ULL : 0ULL;  // 0 = disarmed
+  h2d(peel_prof_buffer() + 15, &w, 1);
+  stream_sync();
+}
+
+void peel_trace_read(unsigned long long* out) {
+  d2h(out, peel_prof_buffer() + 16, kPeelTraceWords);
   stream_sync();
 }
 

@@ -42,7 +42,10 @@
 namespace dgb {
 namespace peelk {
 
-constexpr int PT = 1024;  // threads
+#ifndef DG_PEEL_PT
+#define DG_PEEL_PT 1024
+#endif
+constexpr int PT = DG_PEEL_PT;  // threads (tuning builds: -DDG_PEEL_PT=512)
 constexpr int U = 4;      // arcs in flight per thread (large-batch path)
 constexpr int UQ = 2;     // adjacency quads in flight per thread (small-batch path)
 
@@ -71,10 +74,15 @@ struct Fixed {  // shared-memory tail after keys (and offsets)
   uint64_t ws[33];
   uint64_t wmin[32];
   uint32_t wcnt[32];
+  uint32_t wfirst[32];    // per warp: first vertex at its minimum key,
+  uint32_t wr0[32];       //   its row start (staged offsets only)
+  uint32_t wdeg[32];      //   and its row length
+  uint32_t cnt2[2][32];   // same-batch counters of simple batches, by batch parity
   // warp -> member assignment for batches of 1..32 members:
   // wmap[bs-1][w] = j | rank << 8 | nwj << 16 with j = w % bs, rank = w / bs,
+  // (bs <= #warps)
   // nwj = #warps serving member j (precomputed: no runtime division)
-  uint32_t wmap[32][PT / 32];
+  uint32_t wmap[PT / 32][PT / 32];  // batches of up to one member per warp
 };
 
 template <class K>
@@ -109,14 +117,112 @@ __device__ __forceinline__ uint64_t key_atom(uint64_t* p) {
   return atomicAdd(reinterpret_cast<unsigned long long*>(p), ~0ULL);
 }
 
+// S3 decrement of key u.  ONE: single-member batch (no same-batch arcs,
+// plain reduction); otherwise the returned key counts same-batch
+// neighbours with a smaller id into *cnt.  u32 shared keys address the
+// shared window directly (base hoisted out of the loop).
+template <class K, bool SMEM, bool ONE>
+__device__ __forceinline__ void dec_key(K* keys, uint32_t keys_s, uint32_t u, uint32_t vj,
+                                        uint32_t* cnt) {
+  if constexpr (SMEM && sizeof(K) == 4) {
+    const uint32_t addr = keys_s + (u << 2);
+    if (ONE) {
+      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(0xffffffffu) : "memory");
+    } else {
+      uint32_t old;
+      asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                   : "=r"(old)
+                   : "r"(addr), "r"(0xffffffffu)
+                   : "memory");
+      if (Range<K>::in_batch(K(old)) && u < vj) atomicAdd(cnt, 1u);
+    }
+  } else {
+    if (ONE) {
+      key_red(&keys[u], SMEM);
+    } else {
+      const K old = key_atom(&keys[u]);
+      if (Range<K>::in_batch(old) && u < vj) atomicAdd(cnt, 1u);
+    }
+  }
+}
+
+// timeline stamp (dg_peel_trace_*): lane 0 of every warp, armed window only.
+// `dep` forces the stamp to wait for a preceding shared load.
+__device__ __forceinline__ void stamp(unsigned long long* prof, unsigned long long first,
+                                      unsigned long long nbat, uint32_t w, uint32_t k,
+                                      uint32_t dep) {
+  if (dep == 0xfffffffeu) __trap();
+  const unsigned long long b = nbat + 1 - first;
+  if (b < kPeelTraceBatches)
+    prof[16 + (b * 32 + w) * kPeelTraceStamps + k] = clock64();
+}
+
+// S3 over one member's row for warps [rank] of the nwj serving it: the row
+// [oj, oj + dj) as 16-byte quads indexed relative to its first quad; only the
+// first and last quad can be partial.
+template <class K, bool SMEM, bool ONE, bool TR>
+__device__ __forceinline__ void remove_row(const uint4* adj4, K* keys, uint32_t keys_s,
+                                           uint64_t oj, uint32_t dj, uint32_t vj, uint32_t rank,
+                                           uint32_t nwj, uint32_t lane, uint32_t* cnt,
+                                           unsigned long long* prof = nullptr,
+                                           unsigned long long tr_first = 0,
+                                           unsigned long long nbat = 0, uint32_t w = 0) {
+  const uint4* row = adj4 + (oj >> 2);
+  const uint32_t head = uint32_t(oj & 3), end = head + dj;  // valid elements [head, end)
+  const uint32_t nq = (end + 3) >> 2, stride = nwj * 32;
+  for (uint32_t b = rank * 32 + lane; b < nq; b += stride * UQ) {
+    uint4 x[UQ];
+    const bool tr = TR && tr_first && b - lane == rank * 32;  // warp-uniform: first pass
+    if (tr && lane == 0) stamp(prof, tr_first, nbat, w, 6, 0);
+#pragma unroll
+    for (int k = 0; k < UQ; ++k)
+      if (b + k * stride < nq) x[k] = __ldg(row + b + k * stride);
+    if (TR && tr) {  // probes: every lane's data must have arrived (warp-wide dependency)
+      const uint32_t am = __activemask();  // lanes with b < nq (lane 0 among them)
+      const uint32_t d0 = __reduce_or_sync(am, x[0].x);
+      if (lane == 0) stamp(prof, tr_first, nbat, w, 7, d0 == 0xfffffffeu ? d0 : 0u);
+      uint4 y = make_uint4(0, 0, 0, 0);  // the same quads again, L2 only
+      asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w)
+                   : "l"(row + b));
+      const uint32_t d1 = __reduce_or_sync(am, y.x);
+      if (lane == 0) stamp(prof, tr_first, nbat, w, 8, d1 == 0xfffffffeu ? d1 : 0u);
+      uint4 z = make_uint4(0, 0, 0, 0);  // full-warp quads 256 KB away
+      asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(z.x), "=r"(z.y), "=r"(z.z), "=r"(z.w)
+                   : "l"(row + b + 16 * 1024));
+      const uint32_t d2 = __reduce_or_sync(am, z.x);
+      if (lane == 0) stamp(prof, tr_first, nbat, w, 9, d2 == 0xfffffffeu ? d2 : 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < UQ; ++k) {
+      const uint32_t t = b + k * stride;
+      if (t >= nq) break;
+      const uint32_t e0 = t << 2;
+      if (e0 >= head && e0 + 4 <= end) {
+        dec_key<K, SMEM, ONE>(keys, keys_s, x[k].x, vj, cnt);
+        dec_key<K, SMEM, ONE>(keys, keys_s, x[k].y, vj, cnt);
+        dec_key<K, SMEM, ONE>(keys, keys_s, x[k].z, vj, cnt);
+        dec_key<K, SMEM, ONE>(keys, keys_s, x[k].w, vj, cnt);
+      } else {
+        const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e0 + e >= head && e0 + e < end) dec_key<K, SMEM, ONE>(keys, keys_s, us[e], vj, cnt);
+      }
+    }
+  }
+}
+
 // warp-wide min of a key (redux.sync for 32-bit keys)
 __device__ __forceinline__ uint32_t wmin_key(uint32_t x) { return __reduce_min_sync(~0u, x); }
 __device__ __forceinline__ uint64_t wmin_key(uint64_t x) { return warp_min(x); }
 
-// S1 over a compile-time chunk of 4*VQ u32 keys (VQ > 0) or a runtime chunk.
+// S1 over a compile-time chunk of 4*VQ u32 keys (VQ > 0) or a runtime chunk:
+// min, multiplicity and the first index holding the min.
 template <int VQ, class K>
 __device__ __forceinline__ void chunk_min_count(const K* keys, uint32_t lo, uint32_t c, K& lmin,
-                                                uint32_t& lcnt) {
+                                                uint32_t& lcnt, uint32_t& lfirst) {
   if constexpr (VQ > 0 && sizeof(K) == 4) {
     const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
     uint32_t m = 0xffffffffu;
@@ -125,25 +231,30 @@ __device__ __forceinline__ void chunk_min_count(const K* keys, uint32_t lo, uint
       const uint4 v = kv[q];
       m = min(min(m, min(v.x, v.y)), min(v.z, v.w));
     }
-    uint32_t cnt = 0;
+    uint64_t mask = 0;
 #pragma unroll
     for (int q = 0; q < VQ; ++q) {
       const uint4 v = kv[q];
-      cnt += uint32_t(v.x == m) + uint32_t(v.y == m) + uint32_t(v.z == m) + uint32_t(v.w == m);
+      mask |= uint64_t((v.x == m) | ((v.y == m) << 1) | ((v.z == m) << 2) | ((v.w == m) << 3))
+              << (4 * q);
     }
     lmin = K(m);
-    lcnt = cnt;
+    lcnt = uint32_t(__popcll(mask));
+    lfirst = lo + uint32_t(__ffsll(mask)) - 1;
   } else {
     K m = K(~K(0));
     for (uint32_t i = lo; i < lo + c; ++i) m = min(m, keys[i]);
-    uint32_t cnt = 0;
-    for (uint32_t i = lo; i < lo + c; ++i) cnt += keys[i] == m;
+    uint32_t cnt = 0, first = lo;
+    for (uint32_t i = lo + c; i-- > lo;)
+      if (keys[i] == m) ++cnt, first = i;
     lmin = m;
     lcnt = cnt;
+    lfirst = first;
   }
 }
 
-template <class K, bool SMEM, bool OFFS, int VQ>
+// TR: timeline + cycle counters variant (dg_peel_trace_*, dg_peel_profile)
+template <class K, bool SMEM, bool OFFS, int VQ, bool TR>
 __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
   using R = Range<K>;
   extern __shared__ __align__(16) unsigned char raw_smem[];
@@ -158,9 +269,11 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
   if (OFFS) o += (size_t(npad + 1) * 4 + 15) & ~size_t(15);
   Fixed& s = *reinterpret_cast<Fixed*>(raw_smem + o);
   const uint4* adj4 = reinterpret_cast<const uint4*>(a.adj);
+  const uint32_t keys_s = SMEM ? smem_addr(keys) : 0u;
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
   const uint32_t n = a.n, c = VQ > 0 ? uint32_t(4 * VQ) : a.chunk, lo = tid * c, hi = lo + c;
+  constexpr uint32_t NW = PT / 32;
 
   for (uint32_t i = lo; i < hi; ++i) {
     if (i < n) {
@@ -172,66 +285,39 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
     }
   }
   if (OFFS && tid == 0) soffs[n] = uint32_t(a.offs[n]);
-  for (uint32_t e = tid; e < 32 * (PT / 32); e += PT) {
-    const uint32_t b = e / (PT / 32) + 1, ww = e % (PT / 32);
+  for (uint32_t e = tid; e < NW * NW; e += PT) {
+    const uint32_t b = e / NW + 1, ww = e % NW;
     const uint32_t jj = ww % b;
-    s.wmap[b - 1][ww] = jj | ((ww / b) << 8) | (((PT / 32 - 1 - jj) / b + 1) << 16);
+    s.wmap[b - 1][ww] = jj | ((ww / b) << 8) | (((NW - 1 - jj) / b + 1) << 16);
   }
+  if (tid < 64) (&s.cnt2[0][0])[tid] = 0;
   __syncthreads();
 
+  const unsigned long long tr_first = TR && a.prof ? a.prof[15] : 0;  // 0: timeline disarmed
+#define PK_STAMP(k, dep)                                                 \
+  if constexpr (TR) {                                                    \
+    if (tr_first && lane == 0) stamp(a.prof, tr_first, nbat, w, k, dep); \
+  }
   uint32_t removed = 0, pos = 0, pend_n = 0, pend_pos = 0;
+  uint32_t* pend_cnt = s.cnt;
+  bool pend_reset = false;
   K pend_key = 0;
-  bool marked = false;  // this thread holds BATCH marks of the previous batch
+  bool marked = false;  // my chunk holds BATCH marks of the previous batch
   unsigned long long nbat = 0;
-  long long c_s1 = 0, c_s2 = 0, c_s3 = 0, c_s3_1 = 0, t_mark = clock64();
-  unsigned long long n1 = 0, nbig = 0;
+  long long c_s1 = 0, c_s2 = 0, c_s3 = 0, c_s3_1 = 0, t_mark = TR ? clock64() : 0;
+  unsigned long long n1 = 0, nbig = 0, nsimple = 0;
   while (removed < n) {
-    // ---- deferred raw charges of the previous batch
-    if (tid < pend_n) a.raw[pend_pos + tid] = uint64_t(pend_key) - s.cnt[tid];
-    // ---- S1
-    K lmin;
-    uint32_t lcnt;
-    chunk_min_count<VQ>(keys, lo, c, lmin, lcnt);
-    // Without staged offsets, prefetch the row bounds of my chunk's first
-    // minimum now: if this thread owns the batch, the L2 round trip has
-    // already overlapped barrier A.
-    uint32_t pf_i = 0xffffffffu;
-    uint64_t pf0 = 0, pf1 = 0;
-    if (!OFFS && R::alive(lmin)) {
-      for (uint32_t i = lo; i < hi; ++i)
-        if (keys[i] == lmin) {
-          pf_i = i;
-          break;
-        }
-      if (pf_i != 0xffffffffu) {
-        pf0 = a.offs[pf_i];
-        pf1 = a.offs[pf_i + 1];
-      }
+    PK_STAMP(0, s.wcnt[(w + 1) & 31]);
+    // ---- deferred raw charges of the previous batch (last warp: usually
+    // padding keys only, the first to finish S1)
+    if (tid >= PT - 32 && tid - (PT - 32) < pend_n) {
+      const uint32_t t = tid - (PT - 32);
+      a.raw[pend_pos + t] = uint64_t(pend_key) - pend_cnt[t];
+      if (pend_reset) pend_cnt[t] = 0;
     }
-    if (!R::alive(lmin)) {  // nothing alive in my chunk
-      lmin = R::DEAD;
-      lcnt = 0;
-    }
-    const K wm = wmin_key(lmin);
-    const uint32_t wc = __reduce_add_sync(~0u, lmin == wm ? lcnt : 0u);
-    if (lane == 0) {
-      s.wmin[w] = uint64_t(wm);
-      s.wcnt[w] = wc;
-    }
-    __syncthreads();  // A
-    if (tid == 0) {
-      const long long t = clock64();
-      c_s1 += t - t_mark;
-      t_mark = t;
-    }
-    // ---- S2: global min, batch size, output offsets; write the batch
-    constexpr uint32_t NW = PT / 32;
-    const K xw = lane < NW ? K(s.wmin[lane]) : Range<K>::DEAD;
-    const K gmin = wmin_key(xw);
-    const uint32_t cc = (lane < NW && xw == gmin) ? s.wcnt[lane] : 0u;
-    const uint32_t total = __reduce_add_sync(~0u, cc);
-    const uint32_t bs = a.one ? 1u : total;
-    if (marked) {  // retire my marks of the previous batch
+    // ---- retire my BATCH marks of the previous batch (no decrements run
+    // between barrier C and barrier A, so the read-modify-write is safe)
+    if (marked) {
       if constexpr (VQ > 0 && sizeof(K) == 4) {
         uint4* kv = reinterpret_cast<uint4*>(keys) + (lo >> 2);
 #pragma unroll
@@ -253,178 +339,270 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
       }
       marked = false;
     }
-    if (wm == gmin) {  // this warp owns part of the batch
-      const uint32_t woff = __reduce_add_sync(~0u, lane < w ? cc : 0u);
-      const bool mine = lmin == gmin && lcnt;
-      const uint32_t mm = __ballot_sync(~0u, mine);
-      uint32_t my = woff;
-      if (__popc(mm) > 1) {  // several owners in this warp: lane prefix of counts
-        const uint32_t v = mine ? lcnt : 0u;
-        my += warp_incl_scan(v) - v;
-      }
-      if (mine) {
-        // owner: the chunk's minima in ascending id.  With compile-time chunks
-        // the 128-bit loads are issued up front and matches become a bitmask.
-        uint64_t bits = 0;
-        if constexpr (VQ > 0 && sizeof(K) == 4) {
-          const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
-#pragma unroll
-          for (int q = 0; q < VQ; ++q) {
-            const uint4 v = kv[q];
-            bits |= uint64_t((v.x == gmin) | ((v.y == gmin) << 1) | ((v.z == gmin) << 2) |
-                             ((v.w == gmin) << 3))
-                    << (4 * q);
-          }
-        } else {
-          for (uint32_t i = lo; i < hi && i - lo < 64; ++i)
-            if (keys[i] == gmin) bits |= 1ULL << (i - lo);
-        }
-        uint32_t i_scalar = lo + 64;  // chunks longer than 64 keys continue scalar
-        while (my < bs) {
-          uint32_t i;
-          if (bits) {
-            i = lo + uint32_t(__ffsll(bits) - 1);
-            bits &= bits - 1;
-          } else {
-            while (i_scalar < hi && keys[i_scalar] != gmin) ++i_scalar;
-            if (i_scalar >= hi) break;
-            i = i_scalar++;
-          }
-          a.perm[pos + my] = i;
-          // a single-vertex batch has no same-batch arcs: mark it dead at once
-          keys[i] = bs == 1 ? R::DEAD : R::BATCH;
-          marked = bs != 1;
-          if (my < PT) {
-            uint64_t r0, r1;
-            if (OFFS) {
-              r0 = soffs[i];
-              r1 = soffs[i + 1];
-            } else if (i == pf_i) {
-              r0 = pf0;
-              r1 = pf1;
-            } else {
-              r0 = a.offs[i];
-              r1 = a.offs[i + 1];
-            }
-            s.bv[my] = i;
-            s.boff[my] = r0;
-            s.bdeg[my] = uint32_t(r1 - r0);
-            s.cnt[my] = 0;
-          }
-          ++my;
-        }
+    // ---- S1
+    K lmin = R::DEAD;
+    uint32_t lcnt = 0, lfirst = lo;
+    if (lo < n) chunk_min_count<VQ>(keys, lo, c, lmin, lcnt, lfirst);  // padding: skip
+    if (!R::alive(lmin)) {  // nothing alive in my chunk
+      lmin = R::DEAD;
+      lcnt = 0;
+      lfirst = lo;
+    }
+    // row bounds of my first minimum: staged offsets, or (without them) an
+    // early L2 load whose round trip overlaps barrier A
+    uint64_t r0 = 0, r1 = 0;
+    if (OFFS) {
+      r0 = soffs[lfirst];
+      r1 = soffs[lfirst + 1];
+    } else if (R::alive(lmin)) {
+      r0 = a.offs[lfirst];
+      r1 = a.offs[lfirst + 1];
+    }
+    const K wm = wmin_key(lmin);
+    const uint32_t wc = __reduce_add_sync(~0u, lmin == wm ? lcnt : 0u);
+    if (lane == 0) {
+      s.wmin[w] = uint64_t(wm);
+      s.wcnt[w] = wc;
+    }
+    if (OFFS) {  // the warp's candidate: first lane at the warp minimum
+      const uint32_t fl = __ffs(__ballot_sync(~0u, lmin == wm)) - 1;
+      if (lane == fl) {
+        s.wfirst[w] = lfirst;
+        s.wr0[w] = uint32_t(r0);
+        s.wdeg[w] = uint32_t(r1 - r0);
       }
     }
-    __syncthreads();  // B
-    if (tid == 0) {
-      const long long t = clock64();
-      c_s2 += t - t_mark;
-      t_mark = t;
+    PK_STAMP(1, 0);
+    __syncthreads();  // A
+    if constexpr (TR) {
+      if (tid == 0) {
+        const long long t = clock64();
+        c_s1 += t - t_mark;
+        t_mark = t;
+      }
     }
-    if (bs <= 32) {
-      // ---- S3: warp w serves member j = w mod bs (warp-uniform), its lanes
-      // walk the member's row in 16-byte quads: no prefix scan, no search,
-      // the row bounds are broadcast shared loads.
+    // ---- S2: global min, batch size (every warp reduces the table)
+    const K xw = lane < NW ? K(s.wmin[lane]) : R::DEAD;
+    const uint32_t xc = lane < NW ? s.wcnt[lane] : 0u;
+    const K gmin = wmin_key(xw);
+    const bool own = lane < NW && xw == gmin;
+    const uint32_t ownmask = __ballot_sync(~0u, own);
+    const uint32_t cc = own ? xc : 0u;
+    const uint32_t total = __reduce_add_sync(~0u, cc);
+    const uint32_t bs = a.one ? 1u : total;
+    PK_STAMP(2, uint32_t(gmin) + bs);
+    const bool mine = wm == gmin && lmin == gmin && lcnt;  // my chunk holds members
+    if (OFFS && (a.one || total == uint32_t(__popc(ownmask)))) {
+      // ---- simple batch: every owner warp holds exactly one member (or
+      // one-at-a-time), so the table names the whole batch in ascending id
+      // (owner warps ascend).  No staging, no barrier B.
+      ++nsimple;
+      const uint32_t xf = lane < NW ? s.wfirst[lane] : 0u;
+      const uint32_t xr0 = lane < NW ? s.wr0[lane] : 0u;
+      const uint32_t xd = lane < NW ? s.wdeg[lane] : 0u;
+      // owner lane L (table entry L) holds member rk(L) = #owner lanes below L
+      const uint32_t rk = __popc(ownmask & ((1u << lane) - 1u));
       const uint32_t wm3 = s.wmap[bs - 1][w];
       const uint32_t j = wm3 & 0xffu, rank = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
-      const uint64_t oj = s.boff[j], ej = oj + s.bdeg[j];
-      const uint32_t vj = s.bv[j];
-      const uint64_t q1 = (ej + 3) >> 2, stride = uint64_t(nwj) * 32;
-      for (uint64_t base = (oj >> 2) + uint64_t(rank) * 32; base < q1; base += stride * UQ) {
-        uint4 x[UQ];
-#pragma unroll
-        for (int k = 0; k < UQ; ++k) {
-          const uint64_t q = base + k * stride + lane;
-          if (q < q1) x[k] = __ldg(adj4 + q);
+      const uint32_t lj = __ffs(__ballot_sync(~0u, own && rk == j)) - 1;  // my member's lane
+      if (bs == 1) {
+        if (w == NW - 1 && lane == lj) {
+          a.perm[pos] = xf;
+          keys[xf] = R::DEAD;  // no same-batch arcs: dead at once
         }
-#pragma unroll
-        for (int k = 0; k < UQ; ++k) {
-          const uint64_t q = base + k * stride + lane;
-          if (q >= q1) continue;
-          const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint64_t p = (q << 2) + e;
-            if (p < oj || p >= ej) continue;
-            if (bs == 1) {
-              key_red(&keys[us[e]], SMEM);
-            } else {  // the returned key tells same-batch neighbours apart
-              const K old = key_atom(&keys[us[e]]);
-              if (R::in_batch(old) && us[e] < vj) atomicAdd(&s.cnt[j], 1u);
-            }
-          }
-        }
+      } else {
+        // every warp marks all members before its own decrements, so each of
+        // its atom returns on a member is in the BATCH range (a later mark by
+        // another warp only rewrites a dead key)
+        if (own) keys[xf] = R::BATCH;
+        if (own && w == NW - 1) a.perm[pos + rk] = xf;
+        __syncwarp();
+        marked = mine;
       }
+      const uint32_t vj = __shfl_sync(~0u, xf, lj);
+      const uint32_t oj = __shfl_sync(~0u, xr0, lj), dj = __shfl_sync(~0u, xd, lj);
+      uint32_t* cnt = s.cnt2[nbat & 1];
+      PK_STAMP(3, 0);
+      PK_STAMP(4, vj);
+      if (bs == 1)
+        remove_row<K, SMEM, true, TR>(adj4, keys, keys_s, oj, dj, vj, rank, nwj, lane, nullptr,
+                                      a.prof, tr_first, nbat, w);
+      else
+        remove_row<K, SMEM, false, TR>(adj4, keys, keys_s, oj, dj, vj, rank, nwj, lane,
+                                       &cnt[j], a.prof, tr_first, nbat, w);
+      PK_STAMP(5, 0);
       __syncthreads();  // C
       pend_n = bs;
       pend_pos = pos;
       pend_key = gmin;
+      pend_cnt = cnt;
+      pend_reset = true;
     } else {
-      // ---- S3, large batch: slices of PT members with a CTA scan
-      for (uint32_t s0 = 0; s0 < bs; s0 += PT) {
-        const uint32_t sl = min(uint32_t(PT), bs - s0);
-        if (s0 > 0 && tid < sl) {  // beyond the staged first slice
-          const uint32_t v = a.perm[pos + s0 + tid];
-          const uint64_t r0 = a.offs[v], r1 = a.offs[v + 1];
-          s.bv[tid] = v;
-          s.boff[tid] = r0;
-          s.bdeg[tid] = uint32_t(r1 - r0);
-          s.cnt[tid] = 0;
+      // ---- general batch: owners write the batch in ascending id and stage
+      // (v, row offset, degree) for the CTA
+      if (wm == gmin) {
+        const uint32_t woff = __reduce_add_sync(~0u, lane < w ? cc : 0u);
+        const uint32_t mm = __ballot_sync(~0u, mine);
+        uint32_t my = woff;
+        if (__popc(mm) > 1) {  // several owners in this warp: lane prefix of counts
+          const uint32_t v = mine ? lcnt : 0u;
+          my += warp_incl_scan(v) - v;
         }
-        __syncthreads();
-        const uint64_t d = tid < sl ? s.bdeg[tid] : 0;
-        uint64_t tot;
-        const uint64_t ex = block_excl_scan(d, s.ws, &tot);
-        s.pre[tid] = ex + d;
-        __syncthreads();
-        for (uint64_t b0 = uint64_t(w) * 32 * U; b0 < tot; b0 += uint64_t(PT) * U) {
-          uint32_t u[U], bb[U];
+        if (mine) {
+          // the chunk's minima in ascending id.  With compile-time chunks the
+          // 128-bit loads are issued up front and matches become a bitmask.
+          uint64_t bits = 0;
+          if constexpr (VQ > 0 && sizeof(K) == 4) {
+            const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
 #pragma unroll
-          for (int j = 0; j < U; ++j) {
-            const uint64_t x = b0 + uint64_t(j) * 32 + lane;
-            u[j] = 0xffffffffu;
-            bb[j] = 0;
-            if (x < tot) {
-              uint32_t l = 0, h = sl - 1;
-              while (l < h) {
-                const uint32_t mid = (l + h) >> 1;
-                if (s.pre[mid] > x)
-                  h = mid;
-                else
-                  l = mid + 1;
+            for (int q = 0; q < VQ; ++q) {
+              const uint4 v = kv[q];
+              bits |= uint64_t((v.x == gmin) | ((v.y == gmin) << 1) | ((v.z == gmin) << 2) |
+                               ((v.w == gmin) << 3))
+                      << (4 * q);
+            }
+          } else {
+            for (uint32_t i = lo; i < hi && i - lo < 64; ++i)
+              if (keys[i] == gmin) bits |= 1ULL << (i - lo);
+          }
+          uint32_t i_scalar = lo + 64;  // chunks longer than 64 keys continue scalar
+          while (my < bs) {
+            uint32_t i;
+            if (bits) {
+              i = lo + uint32_t(__ffsll(bits) - 1);
+              bits &= bits - 1;
+            } else {
+              while (i_scalar < hi && keys[i_scalar] != gmin) ++i_scalar;
+              if (i_scalar >= hi) break;
+              i = i_scalar++;
+            }
+            a.perm[pos + my] = i;
+            // a single-vertex batch has no same-batch arcs: mark it dead at once
+            keys[i] = bs == 1 ? R::DEAD : R::BATCH;
+            marked = bs != 1;
+            if (my < PT) {
+              uint64_t q0, q1;
+              if (OFFS) {
+                q0 = soffs[i];
+                q1 = soffs[i + 1];
+              } else if (i == lfirst) {  // the early load of S1
+                q0 = r0;
+                q1 = r1;
+              } else {
+                q0 = a.offs[i];
+                q1 = a.offs[i + 1];
               }
-              bb[j] = l;
-              u[j] = a.adj[s.boff[l] + (x - (l ? s.pre[l - 1] : 0))];
+              s.bv[my] = i;
+              s.boff[my] = q0;
+              s.bdeg[my] = uint32_t(q1 - q0);
+              s.cnt[my] = 0;
+            }
+            ++my;
+          }
+        }
+      }
+      PK_STAMP(3, 0);
+      __syncthreads();  // B
+      if constexpr (TR) {
+        if (tid == 0) {
+          const long long t = clock64();
+          c_s2 += t - t_mark;
+          t_mark = t;
+        }
+      }
+      if (bs <= NW) {
+        // ---- S3: warp w serves member j = w mod bs (warp-uniform), its lanes
+        // walk the member's row in 16-byte quads; row bounds are broadcast
+        // shared loads
+        const uint32_t wm3 = s.wmap[bs - 1][w];
+        const uint32_t j = wm3 & 0xffu, rank = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
+        PK_STAMP(4, wm3);
+        if (bs == 1)
+          remove_row<K, SMEM, true, TR>(adj4, keys, keys_s, s.boff[0], s.bdeg[0], 0, rank, nwj,
+                                        lane, nullptr, a.prof, tr_first, nbat, w);
+        else  // the returned key tells same-batch neighbours apart
+          remove_row<K, SMEM, false, TR>(adj4, keys, keys_s, s.boff[j], s.bdeg[j], s.bv[j], rank,
+                                         nwj, lane, &s.cnt[j], a.prof, tr_first, nbat, w);
+        PK_STAMP(5, 0);
+        __syncthreads();  // C
+        pend_n = bs;
+        pend_pos = pos;
+        pend_key = gmin;
+        pend_cnt = s.cnt;
+        pend_reset = false;
+      } else {
+        // ---- S3, large batch: slices of PT members with a CTA scan
+        for (uint32_t s0 = 0; s0 < bs; s0 += PT) {
+          const uint32_t sl = min(uint32_t(PT), bs - s0);
+          if (s0 > 0 && tid < sl) {  // beyond the staged first slice
+            const uint32_t v = a.perm[pos + s0 + tid];
+            const uint64_t q0 = a.offs[v], q1 = a.offs[v + 1];
+            s.bv[tid] = v;
+            s.boff[tid] = q0;
+            s.bdeg[tid] = uint32_t(q1 - q0);
+            s.cnt[tid] = 0;
+          }
+          __syncthreads();
+          const uint64_t d = tid < sl ? s.bdeg[tid] : 0;
+          uint64_t tot;
+          const uint64_t ex = block_excl_scan(d, s.ws, &tot);
+          s.pre[tid] = ex + d;
+          __syncthreads();
+          for (uint64_t b0 = uint64_t(w) * 32 * U; b0 < tot; b0 += uint64_t(PT) * U) {
+            uint32_t u[U], bb[U];
+#pragma unroll
+            for (int jx = 0; jx < U; ++jx) {
+              const uint64_t x = b0 + uint64_t(jx) * 32 + lane;
+              u[jx] = 0xffffffffu;
+              bb[jx] = 0;
+              if (x < tot) {
+                uint32_t l = 0, h = sl - 1;
+                while (l < h) {
+                  const uint32_t mid = (l + h) >> 1;
+                  if (s.pre[mid] > x)
+                    h = mid;
+                  else
+                    l = mid + 1;
+                }
+                bb[jx] = l;
+                u[jx] = a.adj[s.boff[l] + (x - (l ? s.pre[l - 1] : 0))];
+              }
+            }
+#pragma unroll
+            for (int jx = 0; jx < U; ++jx) {
+              if (u[jx] == 0xffffffffu) continue;
+              const K old = key_atom(&keys[u[jx]]);
+              if (R::in_batch(old) && u[jx] < s.bv[bb[jx]]) atomicAdd(&s.cnt[bb[jx]], 1u);
             }
           }
-#pragma unroll
-          for (int j = 0; j < U; ++j) {
-            if (u[j] == 0xffffffffu) continue;
-            const K old = key_atom(&keys[u[j]]);
-            if (R::in_batch(old) && u[j] < s.bv[bb[j]]) atomicAdd(&s.cnt[bb[j]], 1u);
-          }
+          __syncthreads();
+          if (tid < sl) a.raw[pos + s0 + tid] = uint64_t(gmin) - s.cnt[tid];
+          __syncthreads();
         }
-        __syncthreads();
-        if (tid < sl) a.raw[pos + s0 + tid] = uint64_t(gmin) - s.cnt[tid];
-        __syncthreads();
+        pend_n = 0;
       }
-      pend_n = 0;
     }
-    if (tid == 0) {
-      const long long t = clock64();
-      c_s3 += t - t_mark;
-      if (bs == 1) c_s3_1 += t - t_mark, ++n1;
-      if (bs > 32) ++nbig;
-      t_mark = t;
+    if constexpr (TR) {
+      if (tid == 0) {
+        const long long t = clock64();
+        c_s3 += t - t_mark;
+        if (bs == 1) c_s3_1 += t - t_mark, ++n1;
+        if (bs > NW) ++nbig;
+        t_mark = t;
+      }
     }
     pos += bs;
     removed += bs;
     ++nbat;
   }
-  if (tid < pend_n) a.raw[pend_pos + tid] = uint64_t(pend_key) - s.cnt[tid];
+#undef PK_STAMP
+  if (tid >= PT - 32 && tid - (PT - 32) < pend_n) {
+    const uint32_t t = tid - (PT - 32);
+    a.raw[pend_pos + t] = uint64_t(pend_key) - pend_cnt[t];
+  }
   if (tid == 0) {
     *a.batches = nbat;
-    if (a.prof) {
+    if (TR && a.prof) {
       a.prof[0] = c_s1;
       a.prof[1] = c_s2;
       a.prof[2] = c_s3;
@@ -433,6 +611,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
       a.prof[5] = n1;
       a.prof[6] = nbig;
       a.prof[7] = removed;
+      a.prof[8] = nsimple;
     }
   }
 }

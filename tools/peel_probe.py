@@ -22,6 +22,10 @@ for it in r.trace.iters:
           f"upd={it.update_ms:6.3f}ms us/batch={1e3 * it.order_ms / max(1, it.batches):6.2f} "
           f"arcs/batch={2 * it.m / max(1, it.batches):8.0f}")
 
+# instrumented rerun of the last iteration's core (cycle split; timeline window unreachable)
+dg._chk(dg.LIB.dg_peel_trace_arm(0xFFFFFFF0))
+dg.run(g, dg.RunConfig(iterations=T))
+dg._chk(dg.LIB.dg_peel_trace_arm(0xFFFFFFFF))
 prof = np.zeros(16, np.uint64)
 dg.LIB.dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
 tot = max(1, int(prof[:3].sum()))
@@ -29,7 +33,7 @@ print(f"last peel launch: batches={prof[3]} cycles/batch S1={prof[0]/max(1,prof[
       f"S2={prof[1]/max(1,prof[3]):.0f} S3={prof[2]/max(1,prof[3]):.0f} "
       f"(split {100*prof[0]/tot:.0f}/{100*prof[1]/tot:.0f}/{100*prof[2]/tot:.0f}%) "
       f"single-vertex batches={prof[5]} S3/single={prof[4]/max(1,prof[5]):.0f} "
-      f"S3/multi={(prof[2]-prof[4])/max(1,prof[3]-prof[5]):.0f} big={prof[6]}")
+      f"S3/multi={(prof[2]-prof[4])/max(1,prof[3]-prof[5]):.0f} big={prof[6]} table-path={prof[8]}")
 if len(sys.argv) > 3:  # also time iteration 1's core with the other kernel mode
     mode = int(sys.argv[3])
     dg.set_peel_mode(mode)

@@ -1,0 +1,65 @@
+"""Per-warp timeline of the single-CTA Greedy++ peel (dg_peel_trace_*).
+
+python tools/peel_trace.py [scale] [first_batch]
+
+Runs RMAT-`scale` with T=3 (the trace keeps the last launch: the pruned core
+of iteration 3) and prints, per traced batch, the critical path between the
+three CTA barriers: last arrival and first departure at A / B / C, with the
+warp that arrived last, in SM cycles.
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2311_04333_b200 as dg  # noqa: E402
+
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
+first = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
+u, v = dg.gen_rmat(scale, 16 << scale, scale)
+g = dg.Graph.from_pairs(u, v)
+del u, v
+mode = int(sys.argv[3], 0) if len(sys.argv) > 3 else 0
+dg.set_peel_mode(mode)
+dg._chk(dg.LIB.dg_peel_trace_arm(first))
+r = dg.run(g, dg.RunConfig(iterations=3))
+tr = np.zeros(8 * 32 * 12, np.uint64)
+dg._chk(dg.LIB.dg_peel_trace_read(tr.ctypes.data_as(C.POINTER(C.c_uint64))))
+dg._chk(dg.LIB.dg_peel_trace_arm(0xFFFFFFFF))  # disarm
+tr = tr.reshape(8, 32, 12).astype(np.int64)
+print(f"core n={r.trace.iters[-1].n} batches={r.trace.iters[-1].batches}")
+hdr = ("batch  top->A(last w)  A wait  S2(last w)  B wait  S3(last w)  C wait | total")
+print(hdr)
+tot = np.zeros(7)
+for b in range(7):
+    t = tr[b]
+    nxt = tr[b + 1]
+    top = t[:, 0].min()
+    a_last, a_w = t[:, 1].max(), int(t[:, 1].argmax())
+    a_rel = t[:, 2].min()
+    b_last, b_w = t[:, 3].max(), int(t[:, 3].argmax())
+    has3 = t[:, 4] > 0
+    b_rel = t[has3, 4].min() if has3.any() else b_last
+    c_last = t[has3, 5].max() if has3.any() else b_rel
+    c_w = int(np.where(has3, t[:, 5], 0).argmax())
+    c_rel = nxt[:, 0].min()
+    seg = np.array([a_last - top, a_rel - a_last, b_last - a_rel, b_rel - b_last,
+                    c_last - b_rel, c_rel - c_last, c_rel - top])
+    tot += seg
+    print(f"{first + b:5d}  {seg[0]:6d} (w{a_w:2d})  {seg[1]:6d}  {seg[2]:6d} (w{b_w:2d})  "
+          f"{seg[3]:6d}  {seg[4]:6d} (w{c_w:2d})  {seg[5]:6d} | {seg[6]:6d}")
+print("mean   " + "  ".join(f"{x:8.0f}" for x in tot / 7))
+# S3 detail: per-warp S3 durations of the last traced batch
+b = 5
+print("S3 per warp (batch %d):" % (first + b),
+      [int(tr[b, w, 5] - tr[b, w, 4]) if tr[b, w, 4] else None for w in range(32)])
+ld = [int(tr[b, w, 7] - tr[b, w, 6]) for b in range(7) for w in range(32) if tr[b, w, 6]]
+print("adjacency load latency (cycles, warps with a quad):", "n=%d" % len(ld),
+      "min", min(ld), "median", sorted(ld)[len(ld) // 2], "max", max(ld))
+for k, what in ((8, "same quad again (.cg)"), (9, "cold line 256KB away (.cg)")):
+    x = [int(tr[b, w, k] - tr[b, w, k - 1]) for b in range(7) for w in range(32) if tr[b, w, 6]]
+    print(f"{what}: min {min(x)} median {sorted(x)[len(x) // 2]} max {max(x)}")
+print("S1 per warp (batch %d):" % (first + b),
+      [int(tr[b, w, 1] - tr[b, w, 0]) for w in range(32)])
