@@ -246,7 +246,9 @@ dg_status dg_peel_trace_read(uint64_t out[8 * 32 * 12]);
 dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]);  /* + per-round trace */
 /* Tuning / testing knob for the Greedy++ ordering kernel: 0 automatic (one CTA
  * when the core's keys fit one SM, else a thread-block cluster), 1 single CTA
- * only, 2 cluster whenever it fits.  Results are identical in every mode. */
+ * only, 2 cluster (16 or 8 CTAs) whenever it fits (4- and 2-CTA clusters
+ * measured slower than one CTA on RMAT-22's 35K core).  Results are identical
+ * in every mode. */
 dg_status dg_set_peel_mode(int mode);
 
 #ifdef __cplusplus

@@ -157,6 +157,29 @@ __device__ __forceinline__ void stamp(unsigned long long* prof, unsigned long lo
     prof[16 + (b * 32 + w) * kPeelTraceStamps + k] = clock64();
 }
 
+// adjacency quad of a removed row: each row is read once per launch, so
+// L1 allocation buys nothing (DG_PEEL_LD=1: L2-only .cg loads)
+#ifndef DG_PEEL_LD
+#define DG_PEEL_LD 0
+#endif
+__device__ __forceinline__ uint4 ld_row(const uint4* p) {
+  if constexpr (DG_PEEL_LD == 1) {
+    uint4 r;
+    asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+  } else if constexpr (DG_PEEL_LD == 2) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+  } else {
+    return __ldg(p);
+  }
+}
+
 // S3 over one member's row for warps [rank] of the nwj serving it: the row
 // [oj, oj + dj) as 16-byte quads indexed relative to its first quad; only the
 // first and last quad can be partial.
@@ -176,7 +199,7 @@ __device__ __forceinline__ void remove_row(const uint4* adj4, K* keys, uint32_t 
     if (tr && lane == 0) stamp(prof, tr_first, nbat, w, 6, 0);
 #pragma unroll
     for (int k = 0; k < UQ; ++k)
-      if (b + k * stride < nq) x[k] = __ldg(row + b + k * stride);
+      if (b + k * stride < nq) x[k] = ld_row(row + b + k * stride);
     if (TR && tr) {  // probes: every lane's data must have arrived (warp-wide dependency)
       const uint32_t am = __activemask();  // lanes with b < nq (lane 0 among them)
       const uint32_t d0 = __reduce_or_sync(am, x[0].x);
