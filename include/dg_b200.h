@@ -226,7 +226,14 @@ dg_status dg_flush_l2(void);
 /* Diagnostic latency floors (ns per op): 0 grid barrier (this library's),
  * 1 cooperative-groups grid.sync, 2 cluster barrier (8 CTAs), 3 CTA barrier
  * (1024 threads), 4 dependent L2 load, 5 shared atomicAdd per warp
- * instruction (spread addresses), 6 plain shared load+store per warp instr. */
+ * instruction (spread addresses), 6 plain shared load+store per warp instr,
+ * 7/8 dependent load over 64 MiB / 1 GiB, 9/10 cluster barrier (16 / 4 CTAs),
+ * 11 shared atomic with the result used per warp instruction (spread), 12
+ * spread shared load per warp instruction, 13 / 14 / 15 dependent shared
+ * load / redux.sync / shared atomic chain (one warp, latency per op); 16 / 17
+ * / 18 shared load / reduction / atomic with return at random addresses, 8 in
+ * flight per thread (throughput per warp instruction); 100 + (11..18)
+ * reports SM cycles per op (clock64) instead of ns. */
 dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op);
 /* Diagnostic (instrumented launches only, see dg_peel_trace_arm): thread-0 SM
  * cycles of the last Greedy++ peel launch spent in S1 (min scan), S2 (batch
@@ -244,11 +251,12 @@ dg_status dg_peel_trace_read(uint64_t out[8 * 32 * 12]);
  * scans, level-advance barriers, collects, expansion, flushes, expansion
  * barriers; #level advances; #overflow collects. */
 dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]);  /* + per-round trace */
-/* Tuning / testing knob for the Greedy++ ordering kernel: 0 automatic (one CTA
- * when the core's keys fit one SM, else a thread-block cluster), 1 single CTA
- * only, 2 cluster (16 or 8 CTAs) whenever it fits (4- and 2-CTA clusters
- * measured slower than one CTA on RMAT-22's 35K core).  Results are identical
- * in every mode. */
+/* Tuning / testing knob for the Greedy++ ordering kernel: 0 automatic (batch
+ * mode: the candidate-list kernel for cores above 16K vertices whose keys fit
+ * one SM; then the scanning single-CTA kernel; then a thread-block cluster), 1 scanning
+ * single-CTA kernel only, 2 cluster (16 or 8 CTAs) whenever it fits, 3
+ * candidate-list kernel whenever it fits.  Results are identical in every
+ * mode. */
 dg_status dg_set_peel_mode(int mode);
 
 #ifdef __cplusplus

@@ -490,7 +490,8 @@ def set_device(device: int) -> None:
 
 
 def set_peel_mode(mode: int) -> None:
-    """0 automatic, 1 single-CTA peel only, 2 cluster peel whenever it fits (testing/tuning)."""
+    """0 automatic, 1 scanning single-CTA peel, 2 cluster peel, 3 candidate-list peel
+    (each whenever it fits; testing/tuning -- results are identical)."""
     _chk(LIB.dg_set_peel_mode(mode))
 
 

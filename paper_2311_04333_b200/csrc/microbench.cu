@@ -64,6 +64,75 @@ __global__ void k_mb_atoms(uint64_t iters, uint32_t* sink, int plain) {
   if (a[threadIdx.x] == 0xdeadbeef) *sink = 1;
 }
 
+// shared-memory primitives on one SM: 11 ATOMS with the result used (spread
+// addresses, throughput per warp instruction, 32 warps), 12 LDS at spread
+// addresses (throughput, 32 warps), 13 dependent LDS chain (latency, one
+// warp), 14 dependent redux.sync chain (latency, one warp), 15 dependent
+// ATOMS chain (latency, one warp)
+__global__ void k_mb_smem(int mode, uint64_t iters, uint32_t* sink) {
+  __shared__ uint32_t a[8192];
+  for (uint32_t i = threadIdx.x; i < 8192; i += blockDim.x) a[i] = (i * 40503u + 7919u) & 8191u;
+  __syncthreads();
+  uint32_t idx = (threadIdx.x * 2654435761u) & 8191u, acc = 0;
+  const uint32_t lane = threadIdx.x & 31;
+  const long long t0 = clock64();
+  for (uint64_t i = 0; i < iters; ++i) {
+    if (mode == 11) {
+      acc += atomicAdd(&a[idx], 1u);
+      idx = (idx + 1031u) & 8191u;
+    } else if (mode == 12) {
+      acc += a[idx];
+      idx = (idx + 1031u) & 8191u;
+    } else if (mode == 13) {
+      idx = a[(idx + lane) & 8191u];
+    } else if (mode == 14) {
+      idx = __reduce_min_sync(~0u, idx + lane) + 1u;
+    } else {
+      idx = (atomicAdd(&a[(idx + lane * 33u) & 8191u], 0u) + 1u) & 8191u;
+    }
+  }
+  const long long t1 = clock64();
+  if ((acc ^ idx) == 0xdeadbeefu) *sink = acc;
+  if (threadIdx.x == 0) reinterpret_cast<unsigned long long*>(sink)[1] = (unsigned long long)(t1 - t0);
+}
+
+// throughput with 8 independent ops in flight per thread (32 warps, random
+// bank-spread addresses): 16 LDS, 17 RED (no return), 18 ATOMS (return used
+// after all 8 are issued)
+__global__ void k_mb_smem_tp(int mode, uint64_t iters, uint32_t* sink) {
+  __shared__ uint32_t a[8192];
+  for (uint32_t i = threadIdx.x; i < 8192; i += blockDim.x) a[i] = i;
+  __syncthreads();
+  uint32_t x = threadIdx.x * 2654435761u + 12345u, acc = 0;
+  const long long t0 = clock64();
+  for (uint64_t i = 0; i < iters; ++i) {
+    uint32_t idx[8], r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x = x * 1664525u + 1013904223u;
+      idx[k] = x >> 19;  // random over 8192 words
+    }
+    if (mode == 16) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = a[idx[k]];
+    } else if (mode == 17) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) atomicAdd(&a[idx[k]], 1u);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = 0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = atomicAdd(&a[idx[k]], 1u);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += r[k];
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (acc == 0xdeadbeefu) *sink = acc;
+  if (threadIdx.x == 0) reinterpret_cast<unsigned long long*>(sink)[1] = (unsigned long long)(t1 - t0);
+}
+
 __global__ void k_mb_init_chase(uint32_t* next, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     next[i] = uint32_t((uint64_t(i) * 40503u + 7919u) % n);  // full-cycle-ish stride walk
@@ -76,7 +145,9 @@ using namespace dgb;
 
 extern "C" dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op) {
   try {
-    DevBuf<uint32_t> sink(1);
+    const bool g_mb_cycles = which >= 111 && which <= 118;  // 100 + mode: SM cycles per op
+    if (g_mb_cycles) which -= 100;
+    DevBuf<uint32_t> sink(4);  // [0] sink, [2..3] SM cycles of the timed loop (smem modes)
     cudaEvent_t e0, e1;
     DG_CUDA(cudaEventCreate(&e0));
     DG_CUDA(cudaEventCreate(&e1));
@@ -122,6 +193,10 @@ extern "C" dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op)
       DG_CUDA(cudaLaunchKernelEx(&cfg, k_mb_cluster_dyn, iters));
     } else if (which == 5 || which == 6) {
       k_mb_atoms<<<1, 1024, 0, stream()>>>(iters, sink.get(), which == 6);
+    } else if (which >= 16 && which <= 18) {
+      k_mb_smem_tp<<<1, 1024, 0, stream()>>>(which, iters, sink.get());
+    } else if (which >= 11 && which <= 15) {
+      k_mb_smem<<<1, which <= 12 ? 1024 : 32, 0, stream()>>>(which, iters, sink.get());
     } else {
       throw DgError(DG_E_PARAM, "unknown microbenchmark");
     }
@@ -134,8 +209,16 @@ extern "C" dg_status dg_microbench(int which, uint64_t iters, double* ns_per_op)
     cudaEventDestroy(e1);
     // per op: barriers per iteration; atomics per warp-instruction (32 lanes x 32 warps)
     double ops = double(iters);
-    if (which == 5 || which == 6) ops = double(iters) * 32;  // warp instructions per SM
+    if (which == 5 || which == 6 || which == 11 || which == 12)
+      ops = double(iters) * 32;  // warp instructions per SM
+    if (which >= 16 && which <= 18) ops = double(iters) * 32 * 8;
     *ns_per_op = ms * 1e6 / ops;
+    if (g_mb_cycles && which >= 11 && which <= 18) {
+      unsigned long long cyc = 0;
+      d2h(&cyc, reinterpret_cast<unsigned long long*>(sink.get()) + 1, 1);
+      stream_sync();
+      *ns_per_op = double(cyc) / ops;  // SM cycles per op instead of ns
+    }
     return DG_OK;
   } catch (const DgError& e) {
     return e.code;
@@ -188,7 +271,7 @@ namespace dgb {
 extern int g_peel_mode;
 }
 extern "C" dg_status dg_set_peel_mode(int mode) {
-  if (mode < 0 || mode > 2) return DG_E_PARAM;
+  if (mode < 0 || mode > 3) return DG_E_PARAM;
   dgb::g_peel_mode = mode;
   return DG_OK;
 }

@@ -314,10 +314,11 @@ def test_cpp_dropin_api_on_device():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_peel_kernel_modes_agree(dg, orc, golden, mode):
-    """The single-CTA (mode 1) and the thread-block-cluster (mode 2) Greedy++
-    kernels must both reproduce the reference bit for bit."""
+    """The scanning single-CTA (mode 1), thread-block-cluster (mode 2) and
+    candidate-list (mode 3) Greedy++ kernels must all reproduce the reference
+    bit for bit."""
     dg.set_peel_mode(mode)
     try:
         for c in golden["peel"][::3]:
@@ -344,5 +345,39 @@ def test_peel_kernel_modes_agree(dg, orc, golden, mode):
         assert (r.best.edges, r.best.verts) == o.best and np.array_equal(r.witness, o.witness)
         assert [(t.iter, t.rho.edges, t.rho.verts, t.n, t.m, t.width)
                 for t in r.trace.iters] == o.trace
+    finally:
+        dg.set_peel_mode(0)
+
+
+@pytest.mark.gpu
+def test_peel_queue_paths(dg, orc):
+    """Candidate-list kernel corner paths against the oracle's batch peel
+    (refine.cpp:20-156): a tie group larger than the member staging (ordered
+    full-scan batch), widely spread loads (frequent window rebases), many
+    large batches (slice removal) and loads whose keys cross the window."""
+    rng = np.random.default_rng(7)
+    cases = []
+    # K_{1500,40}: 1500 vertices tie at key 40 > 1024 staged members
+    e = [(a, 1500 + b) for a in range(1500) for b in range(40)]
+    u, v = np.array([x for x, _ in e], np.uint64), np.array([y for _, y in e], np.uint64)
+    cases.append((u, v, None))
+    gu, gv = orc.gen_gnp(4000, 8, 11)
+    cases.append((gu, gv, rng.integers(0, 1 << 20, 4000).astype(np.uint64)))
+    cases.append((gu, gv, rng.integers(0, 64, 4000).astype(np.uint64)))
+    ru, rv = orc.gen_rmat(14, 8 << 14, 5)
+    cases.append((ru, rv, None))
+    dg.set_peel_mode(3)
+    try:
+        for u, v, loads in cases:
+            g = dg.Graph.from_pairs(u, v)
+            h = orc.build(u, v)
+            ld = np.zeros(g.n, np.uint64) if loads is None else loads[: g.n].copy()
+            lh = ld.copy()
+            for _ in range(3):
+                p = dg.load_peel_order(g, ld).perm
+                assert np.array_equal(p, orc.peel_order(h, lh))
+                dg.density_and_load_update(g, p, ld)
+                _, lh, _, _ = orc.density_update(h, p, lh)
+                assert np.array_equal(ld, lh)
     finally:
         dg.set_peel_mode(0)

@@ -38,7 +38,7 @@ for b in range(7):
     nxt = tr[b + 1]
     top = t[:, 0].min()
     a_last, a_w = t[:, 1].max(), int(t[:, 1].argmax())
-    a_rel = t[:, 2].min()
+    a_rel = t[t[:, 2] > 0, 2].min()
     b_last, b_w = t[:, 3].max(), int(t[:, 3].argmax())
     has3 = t[:, 4] > 0
     b_rel = t[has3, 4].min() if has3.any() else b_last
@@ -55,11 +55,12 @@ print("mean   " + "  ".join(f"{x:8.0f}" for x in tot / 7))
 b = 5
 print("S3 per warp (batch %d):" % (first + b),
       [int(tr[b, w, 5] - tr[b, w, 4]) if tr[b, w, 4] else None for w in range(32)])
-ld = [int(tr[b, w, 7] - tr[b, w, 6]) for b in range(7) for w in range(32) if tr[b, w, 6]]
-print("adjacency load latency (cycles, warps with a quad):", "n=%d" % len(ld),
-      "min", min(ld), "median", sorted(ld)[len(ld) // 2], "max", max(ld))
-for k, what in ((8, "same quad again (.cg)"), (9, "cold line 256KB away (.cg)")):
-    x = [int(tr[b, w, k] - tr[b, w, k - 1]) for b in range(7) for w in range(32) if tr[b, w, 6]]
-    print(f"{what}: min {min(x)} median {sorted(x)[len(x) // 2]} max {max(x)}")
+# generic segment medians (both stamps set, same warp): see the stamp map in
+# the kernels (peel_kernel.cuh / peel_queue.cuh, PK_STAMP / PQ_STAMP)
+for a_, b_ in ((0, 6), (6, 7), (7, 8), (8, 9), (8, 1), (9, 1), (1, 2), (2, 3), (3, 4), (4, 5), (6, 8)):
+    x = sorted(int(tr[b, w, b_] - tr[b, w, a_]) for b in range(7) for w in range(32)
+               if tr[b, w, a_] and tr[b, w, b_] and tr[b, w, b_] >= tr[b, w, a_])
+    if x:
+        print(f"  stamp {a_}->{b_}: n={len(x)} median {x[len(x) // 2]} p90 {x[9 * len(x) // 10]}")
 print("S1 per warp (batch %d):" % (first + b),
-      [int(tr[b, w, 1] - tr[b, w, 0]) for w in range(32)])
+      [int(tr[b, w, 1] - tr[b, w, 0]) if tr[b, w, 1] else None for w in range(32)])
