@@ -381,3 +381,43 @@ def test_peel_queue_paths(dg, orc):
                 assert np.array_equal(ld, lh)
     finally:
         dg.set_peel_mode(0)
+
+
+@pytest.mark.gpu
+def test_full_size_rmat22_vs_oracle(dg, orc):
+    """The bench configuration itself (BASELINE configs[1]: RMAT-22, seed 22,
+    67M samples) bit-exact against the oracle: CSR, coreness (labels, kmax,
+    peel_rounds), and a T=3 run -- iteration 1 on the 35K core takes the
+    candidate-list kernel, later ones the scanning kernel.  Plus properties
+    that hold at any size: every vertex of label k has >= k neighbours of
+    label >= k, and the loads gain exactly m per Greedy++ iteration."""
+    u, v = dg.gen_rmat(22, 16 << 22, 22)
+    hu, hv = orc.gen_rmat(22, 16 << 22, 22)
+    assert np.array_equal(u, hu) and np.array_equal(v, hv)
+    del hu, hv
+    g = dg.Graph.from_pairs(u, v)
+    h = orc.build(u, v)
+    del u, v
+    assert same_csr(g, h)
+    d = dg.exact_coreness(g)
+    lab, kmax, rounds = orc.coreness(h)
+    assert np.array_equal(d.labels, lab) and (d.kmax, d.peel_rounds) == (kmax, rounds)
+    # k-core certificate: label(u) >= label(v) for at least label(v) neighbours
+    src = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(h.offs).astype(np.int64))
+    hi = (lab[h.adj] >= lab[src]).astype(np.int64)
+    support = np.bincount(src, weights=hi, minlength=g.n)
+    assert np.all(support >= lab)
+    del src, hi, support
+    r = dg.run(g, dg.RunConfig(iterations=3))
+    o = orc.run(h, ORunConfig(iterations=3))
+    assert (r.best.edges, r.best.verts) == o.best and np.array_equal(r.witness, o.witness)
+    assert [(t.iter, t.rho.edges, t.rho.verts, t.n, t.m, t.width)
+            for t in r.trace.iters] == o.trace
+    assert np.array_equal(r.trace.final_vertices, o.final_vertices)
+    core = dg.get_core(g, d, (d.kmax + 1) // 2)
+    loads = np.zeros(core.n, np.uint64)
+    for it in range(1, 3):
+        p = dg.load_peel_order(core, loads).perm
+        assert np.array_equal(np.sort(p), np.arange(core.n, dtype=p.dtype))
+        dg.density_and_load_update(core, p, loads)
+        assert int(loads.sum()) == it * core.m
