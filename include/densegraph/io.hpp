@@ -11,6 +11,7 @@
 #include <cstring>
 #include <fstream>
 #include <istream>
+#include <iterator>
 #include <ostream>
 #include <string>
 #include <vector>
@@ -25,39 +26,24 @@ struct ParseOptions {
   char comment = '#';
 };
 
+// Tokenised on the device (dg_parse_edge_list, csrc/parse.cu) with the
+// reference's rules; the message of a ParseError carries the line's text.
 inline Graph parse_edge_list(std::istream& in, const ParseOptions& opts = {}) {
-  std::vector<u64> us, vs;
-  std::string line;
-  std::size_t lineno = 0;
-  while (std::getline(in, line)) {
-    ++lineno;
-    if (!line.empty() && line.back() == '\r') line.pop_back();
-    const std::size_t first = line.find_first_not_of(" \t");
-    if (first == std::string::npos || line[first] == opts.comment) continue;
-    u64 id[2];
-    int got = 0;
-    const char* p = line.data() + first;
-    const char* end = line.data() + line.size();
-    while (p < end) {
-      const char* q = p;
-      while (q < end && *q != ' ' && *q != '\t') ++q;
-      u64 x = 0;
-      auto [ptr, ec] = std::from_chars(p, q, x);
-      if (got == 2 || ec != std::errc() || ptr != q)
-        throw ParseError(lineno, "expected two non-negative integers, got \"" + line + "\"");
-      id[got++] = x;
-      p = q;
-      while (p < end && (*p == ' ' || *p == '\t')) ++p;
-    }
-    if (got != 2)
-      throw ParseError(lineno, "expected two non-negative integers, got \"" + line + "\"");
-    us.push_back(id[0]);
-    vs.push_back(id[1]);
-  }
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
   if (in.bad()) throw IoError("read failure while parsing edge list");
-  if (us.empty()) throw EmptyGraphError("no edges after removing self-loops and duplicates");
   dg_graph* h = nullptr;
-  detail::check(dg_graph_build(us.data(), vs.data(), us.size(), 0, &h));
+  uint64_t bad = 0;
+  const dg_status st =
+      dg_parse_edge_list(text.data(), text.size(), opts.comment, 0, &h, &bad);
+  if (st == DG_E_PARSE && bad) {
+    std::size_t b = 0;
+    for (uint64_t l = 1; l < bad; ++l) b = text.find('\n', b) + 1;
+    std::size_t e = text.find('\n', b);
+    std::string line = text.substr(b, e == std::string::npos ? std::string::npos : e - b);
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    throw ParseError(std::size_t(bad), "expected two non-negative integers, got \"" + line + "\"");
+  }
+  detail::check(st);
   return Graph::from_device(h);
 }
 

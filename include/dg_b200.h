@@ -61,6 +61,14 @@ dg_status dg_graph_build(const uint64_t* u, const uint64_t* v, uint64_t k, int o
 
 /* Wrap an existing CSR (Graph{n,m,offs,adj,orig}, graph.hpp:24-30). Copies
  * host arrays (on_device == 0) or device arrays (on_device != 0). */
+/* parse_edge_list(istream&, ParseOptions) (io.hpp:18-19, io.cpp:25-94): edge-
+ * list text (len bytes, host or device memory) tokenised ON THE DEVICE with
+ * the reference's rules, then the CSR build of dg_graph_build.  Malformed
+ * input returns DG_E_PARSE with *bad_line = the 1-based number of the first
+ * malformed line (the caller formats ParseError's message with its text);
+ * no edge left returns DG_E_EMPTY. */
+dg_status dg_parse_edge_list(const char* text, uint64_t len, char comment, int on_device,
+                             dg_graph** out, uint64_t* bad_line);
 dg_status dg_graph_from_csr(uint64_t n, const uint64_t* offs, const uint32_t* adj,
                             const uint64_t* orig, int on_device, dg_graph** out);
 

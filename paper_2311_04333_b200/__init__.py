@@ -28,7 +28,7 @@ from ._abi import LIB, DgIterRecord, DgOutcome, DgRunConfig, DgRunResult, u8p, u
 __all__ = [
     "Density", "Graph", "GraphStats", "CoreDecomposition", "LoadState", "Ordering",
     "RefineOutcome", "RunConfig", "RunResult", "RunTrace", "IterRecord", "InitRecord",
-    "parse_edge_list", "induced_subgraph", "exact_coreness", "approx_coreness", "get_core",
+    "parse_edge_list", "parse_edge_list_file", "induced_subgraph", "exact_coreness", "approx_coreness", "get_core",
     "load_peel_order", "load_sort_order", "density_and_load_update", "charikar_peel",
     "slack_violations", "default_iterations", "run", "gen_rmat", "gen_chung_lu",
     "DensegraphError", "ParseError", "EmptyGraphError", "IoError", "ParamError",
@@ -253,27 +253,35 @@ class Graph:
         return Density(self.m, self.n if self.n else 1)
 
 
-def parse_edge_list(text: str, comment: str = "#") -> Graph:
-    """parse_edge_list(istream) (io.hpp:18, io.cpp:25-94): tokenising on the host
-    (not on the hot path), CSR build on the device."""
-    us, vs = [], []
-    for lineno, line in enumerate(text.split("\n"), 1):
-        if line.endswith("\r"):
+def parse_edge_list(text, comment: str = "#") -> Graph:
+    """parse_edge_list(istream) (io.hpp:18, io.cpp:25-94): the text is
+    tokenised on the device with the reference's rules (csrc/parse.cu), then
+    built into the CSR.  `text` is str (UTF-8 bytes, as read from a file) or
+    bytes.  Errors are the reference's: ParseError at the first malformed line
+    (its text, one trailing CR dropped), EmptyGraphError when no edge is left."""
+    raw = bytes(text) if isinstance(text, (bytes, bytearray)) else text.encode("utf-8")
+    h, bad = C.c_void_p(), C.c_uint64()
+    st = LIB.dg_parse_edge_list(raw, len(raw), comment.encode("latin-1")[:1], 0, C.byref(h),
+                                C.byref(bad))
+    if st == ParseError.code and bad.value:
+        line = raw.split(b"\n")[bad.value - 1]
+        if line.endswith(b"\r"):
             line = line[:-1]
-        s = line.lstrip(" \t")
-        if not s or s[0] == comment:
-            continue
-        toks = [t for t in s.replace("\t", " ").split(" ") if t]
-        if len(toks) != 2 or not all(t.isdigit() for t in toks):
-            raise ParseError(lineno, f'expected two non-negative integers, got "{line}"')
-        a, b = int(toks[0]), int(toks[1])
-        if a >= 1 << 64 or b >= 1 << 64:
-            raise ParseError(lineno, f'expected two non-negative integers, got "{line}"')
-        us.append(a)
-        vs.append(b)
-    if not any(a != b for a, b in zip(us, vs)):
-        raise EmptyGraphError("no edges after removing self-loops and duplicates")
-    return Graph.from_pairs(np.array(us, np.uint64), np.array(vs, np.uint64))
+        shown = line.decode("latin-1") if isinstance(text, (bytes, bytearray)) else line.decode(
+            "utf-8", "replace")
+        raise ParseError(bad.value, f'expected two non-negative integers, got "{shown}"')
+    _chk(st)
+    return Graph(h)
+
+
+def parse_edge_list_file(path: str, comment: str = "#") -> Graph:
+    """parse_edge_list_file (io.hpp:19, io.cpp:96-100)."""
+    try:
+        with open(path, "rb") as f:
+            raw = f.read()
+    except OSError as e:
+        raise IoError(f"cannot open {path}") from e
+    return parse_edge_list(raw, comment)
 
 
 def induced_subgraph(g: Graph, keep, old_to_new: bool = False):

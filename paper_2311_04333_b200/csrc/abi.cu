@@ -419,6 +419,25 @@ dg_status dg_graph_build(const uint64_t* u, const uint64_t* v, uint64_t k, int o
   DG_API_END
 }
 
+dg_status dg_parse_edge_list(const char* text, uint64_t len, char comment, int on_device,
+                             dg_graph** out, uint64_t* bad_line) {
+  DG_API_BEGIN
+  if (!out || !bad_line || (len && !text)) throw DgError(DG_E_PARAM, "null argument");
+  *out = nullptr;
+  *bad_line = 0;
+  GraphPtr g;
+  const uint8_t* t = reinterpret_cast<const uint8_t*>(text);
+  if (on_device) {
+    g = parse_edge_list(t, len, uint8_t(comment), bad_line);
+  } else {
+    DevBuf<uint8_t> d = stage(t, len, 0);
+    g = parse_edge_list(d.get(), len, uint8_t(comment), bad_line);
+  }
+  stream_sync();
+  *out = g.release();
+  DG_API_END
+}
+
 dg_status dg_graph_from_csr(uint64_t n, const uint64_t* offs, const uint32_t* adj,
                             const uint64_t* orig, int on_device, dg_graph** out) {
   DG_API_BEGIN

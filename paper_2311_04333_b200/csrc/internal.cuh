@@ -20,6 +20,8 @@ using GraphPtr = std::unique_ptr<dg_graph>;
 
 // ---- graph.cu ----
 GraphPtr build_from_pairs(const uint64_t* d_u, const uint64_t* d_v, uint64_t k);
+// parse.cu: edge-list text on the device -> CSR (DG_E_PARSE sets *bad_line)
+GraphPtr parse_edge_list(const uint8_t* d_text, uint64_t len, uint8_t comment, uint64_t* bad_line);
 GraphPtr graph_from_device_csr(uint64_t n, const uint64_t* d_offs, const uint32_t* d_adj,
                                const uint64_t* d_orig);
 uint64_t device_max_degree(const uint64_t* d_offs, uint64_t n);

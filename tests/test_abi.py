@@ -60,15 +60,15 @@ def test_density_helpers():
         dg.ceil_div(1, 0)
 
 
-def test_parse_edge_list_host_tokenizer_errors():
+def test_parse_edge_list_fails_loudly_without_gpu():
+    """Tokenising runs on the device (csrc/parse.cu): with no GPU the call
+    raises instead of falling back to a host parser."""
+    import torch
     import paper_2311_04333_b200 as dg
-    with pytest.raises(dg.ParseError) as e:
-        dg.parse_edge_list("0 1\n1 x\n")
-    assert e.value.line == 2
-    with pytest.raises(dg.ParseError):
-        dg.parse_edge_list("0 1 2\n")
-    with pytest.raises(dg.EmptyGraphError):
-        dg.parse_edge_list("# nothing\n3 3\n")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(dg.CudaError):
+        dg.parse_edge_list("0 1\n1 2\n")
 
 
 def test_cpp_dropin_headers_compile():

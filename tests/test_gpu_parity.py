@@ -6,6 +6,7 @@ peel_rounds, Greedy++ permutations (batch and one-at-a-time), per-iteration
 loads, suffix densities, widths, run traces, witnesses, final vertex sets.
 """
 import hashlib
+import json
 import os
 import subprocess
 
@@ -421,3 +422,46 @@ def test_full_size_rmat22_vs_oracle(dg, orc):
         assert np.array_equal(np.sort(p), np.arange(core.n, dtype=p.dtype))
         dg.density_and_load_update(core, p, loads)
         assert int(loads.sum()) == it * core.m
+
+
+def _parse_fixtures():
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "parse.json")) as f:
+        return json.load(f)
+
+
+def test_parse_edge_list_vs_reference_fixtures(dg):
+    """Device tokeniser (csrc/parse.cu) against the reference parser's own
+    outcomes (tests/golden/parse.json, made by make_parse_golden.py from
+    io.cpp:25-94): CSR arrays, or the status and exact message."""
+    for c in _parse_fixtures():
+        raw = c["text"].encode("latin-1")
+        if c["status"] == 0:
+            g = dg.parse_edge_list(raw)
+            assert (g.n, g.m) == (c["n"], c["m"]), c["name"]
+            assert (sha(g.offs), sha(g.adj), sha(g.orig)) == (c["offs"], c["adj"], c["orig"]), c["name"]
+            continue
+        err = {1: dg.ParseError, 2: dg.EmptyGraphError}[c["status"]]
+        with pytest.raises(err) as e:
+            dg.parse_edge_list(raw)
+        # the reference message passes a C string: compare up to a NUL byte
+        assert str(e.value).split("\0")[0] == c["message"], c["name"]
+
+
+def test_parse_edge_list_at_scale(dg, orc, tmp_path):
+    """RMAT-18 pairs written as text (mixed blanks, CRLF, comments) parse on the
+    device into the oracle's CSR; the file and stream entry points agree."""
+    u, v = orc.gen_rmat(18, 16 << 18, 181)
+    rng = np.random.default_rng(5)
+    sep = rng.choice(np.array([" ", "\t", "  "]), len(u))
+    eol = rng.choice(np.array(["\n", "\r\n"]), len(u))
+    lines = np.char.add(np.char.add(np.char.add(u.astype(str), sep), v.astype(str)), eol)
+    text = "# rmat18\n" + "".join(lines.tolist())
+    g = dg.parse_edge_list(text)
+    h = orc.build(u, v)
+    assert same_csr(g, h)
+    p = tmp_path / "g.txt"
+    p.write_text(text)
+    g2 = dg.parse_edge_list_file(str(p))
+    assert (sha(g2.offs), sha(g2.adj)) == (sha(g.offs), sha(g.adj))
+    with pytest.raises(dg.IoError):
+        dg.parse_edge_list_file(str(tmp_path / "missing.txt"))
