@@ -27,27 +27,57 @@ constexpr uint32_t PW = 256;  // window bytes per thread
 
 __device__ __forceinline__ bool blank(uint8_t c) { return c == ' ' || c == '\t'; }
 
-// 0: skip, 1: pair (a, b), 2: malformed.  [p, e) is the line without '\n'.
-__device__ int parse_line(const uint8_t* __restrict__ t, uint64_t p, uint64_t e, uint8_t comment,
-                          uint64_t& a, uint64_t& b) {
-  if (e > p && t[e - 1] == '\r') --e;
+// One forward scan per line from its first byte p: returns the start of the
+// next line in *next and 0: skip, 1: pair (a, b), 2: malformed.  A '\r' ends
+// the line only when '\n' or the end of the text follows (the reference drops
+// ONE trailing '\r' before tokenising); anywhere else it is a token byte.
+// u64 overflow (from_chars out_of_range) is two comparisons, no division.
+__device__ __forceinline__ int parse_line(const uint8_t* __restrict__ t, uint64_t len, uint64_t p,
+                                          uint8_t comment, uint64_t& a, uint64_t& b,
+                                          uint64_t* next) {
+  constexpr uint64_t kCut = 0xffffffffffffffffULL / 10;  // 1844674407370955161
   uint64_t q = p;
-  while (q < e && blank(t[q])) ++q;
-  if (q == e || t[q] == comment) return 0;
+  auto at_eol = [&](uint64_t i) {  // line end at i (excluding a trailing CR)
+    if (i >= len) return true;
+    const uint8_t c = __ldg(t + i);
+    return c == '\n' || (c == '\r' && (i + 1 >= len || __ldg(t + i + 1) == '\n'));
+  };
+  auto skip_line = [&](uint64_t i) {
+    while (i < len && __ldg(t + i) != '\n') ++i;
+    *next = i + 1;
+  };
+  while (!at_eol(q) && blank(__ldg(t + q))) ++q;
+  if (at_eol(q)) {
+    skip_line(q);
+    return 0;
+  }
+  if (__ldg(t + q) == comment) {
+    skip_line(q);
+    return 0;
+  }
   uint64_t id[2] = {0, 0};
   int tok = 0;
-  while (q < e) {
-    if (tok == 2) return 2;  // a third token
+  while (!at_eol(q)) {
+    if (tok == 2) {  // a third token
+      skip_line(q);
+      return 2;
+    }
     uint64_t x = 0;
-    for (; q < e && !blank(t[q]); ++q) {
-      const uint32_t d = uint32_t(t[q]) - '0';
-      if (d > 9) return 2;
-      if (x > (0xffffffffffffffffULL - d) / 10) return 2;  // from_chars: out of range
+    while (!at_eol(q)) {
+      const uint8_t c = __ldg(t + q);
+      if (blank(c)) break;
+      const uint32_t d = uint32_t(c) - '0';
+      if (d > 9 || x > kCut || (x == kCut && d > 5)) {
+        skip_line(q);
+        return 2;
+      }
       x = x * 10 + d;
+      ++q;
     }
     id[tok++] = x;
-    while (q < e && blank(t[q])) ++q;
+    while (!at_eol(q) && blank(__ldg(t + q))) ++q;
   }
+  skip_line(q);
   if (tok != 2) return 2;
   if (id[0] == id[1]) return 0;  // self-loop
   a = id[0];
@@ -64,16 +94,14 @@ __global__ void k_parse(const uint8_t* __restrict__ t, uint64_t len, uint8_t com
        w += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t w0 = w * PW, w1 = min(w0 + PW, len);
     uint64_t p = w0;
-    if (p > 0 && t[p - 1] != '\n') {  // the line in progress belongs to an earlier window
-      while (p < w1 && t[p] != '\n') ++p;
+    if (p > 0 && __ldg(t + p - 1) != '\n') {  // the line in progress belongs to an earlier window
+      while (p < w1 && __ldg(t + p) != '\n') ++p;
       ++p;
     }
     uint64_t c = 0, o = WRITE ? off[w] : 0;
     while (p < w1) {
-      uint64_t e = p;
-      while (e < len && t[e] != '\n') ++e;
-      uint64_t a, b;
-      const int k = parse_line(t, p, e, comment, a, b);
+      uint64_t a, b, nx;
+      const int k = parse_line(t, len, p, comment, a, b, &nx);
       if (k == 1) {
         if (WRITE) {
           pu[o + c] = a;
@@ -83,7 +111,7 @@ __global__ void k_parse(const uint8_t* __restrict__ t, uint64_t len, uint8_t com
       } else if (k == 2 && !WRITE) {
         atomicMin(bad, (unsigned long long)p);
       }
-      p = e + 1;
+      p = nx;
     }
     if (!WRITE) cnt[w] = c;
   }
