@@ -46,6 +46,8 @@ struct alignas(128) Acc {  // one cache line each: no false sharing between phas
   unsigned long long live;   // live-list entries written
   uint32_t minv;             // min alive degree (level advance)
   uint32_t ovf;              // some CTA buffer overflowed while building
+  unsigned long long live2;  // live-list entries of a fallback collect (level advance)
+  uint32_t cov;              // a CTA's level-advance candidate buffer overflowed
 };
 
 struct Frontier {
@@ -77,6 +79,7 @@ struct Smem {
   uint32_t id[BUF];
   uint32_t dg[BUF];
   uint64_t of[BUF];
+  uint32_t rd[BUF];  // residual degree of a level-advance candidate
   uint64_t tileA[KC_THREADS];
   uint64_t ws[33];
   uint32_t ws32[33];
@@ -84,15 +87,22 @@ struct Smem {
   unsigned long long baseF, baseL;
   // phase scalars fetched by thread 0 after each grid barrier
   uint32_t abort;
-  unsigned long long b_front, b_live;
-  uint32_t b_minv, b_ovf;
+  unsigned long long b_front, b_live, b_live2;
+  uint32_t b_minv, b_ovf, b_cov;
+  uint32_t lcov;  // this CTA's candidate buffer overflowed (level advance)
 };
+
+// Level advance candidates: alive vertices within LW of the current bound are
+// staged during the min scan, so the usual small jump needs no second pass.
+constexpr uint32_t LW = 16;
 
 __device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
   s.b_front = ld_relaxed_u64(&acc->front);
   s.b_live = ld_relaxed_u64(&acc->live);
   s.b_minv = ld_relaxed_u32(&acc->minv);
   s.b_ovf = ld_relaxed_u32(&acc->ovf);
+  s.b_live2 = ld_relaxed_u64(&acc->live2);
+  s.b_cov = ld_relaxed_u32(&acc->cov);
 }
 
 // All threads of the CTA call this with a per-thread candidate (isF, v, d, o).
@@ -141,7 +151,7 @@ __device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d
 // the other alive ones are compacted into live_out.
 __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const uint32_t* live_in,
                         uint32_t* live_out, uint32_t bound, uint32_t label, const Frontier& F,
-                        Acc* acc, Smem& s) {
+                        Acc* acc, Smem& s, unsigned long long* live_ctr) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < livec; base += stride) {
     const uint64_t i = base + threadIdx.x;
@@ -162,7 +172,7 @@ __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const ui
     }
     uint32_t totL;
     const uint32_t exL = block_excl_scan<uint32_t>(isL ? 1u : 0u, s.ws32, &totL);
-    if (threadIdx.x == 0 && totL) s.baseL = atomicAdd(&acc->live, (unsigned long long)totL);
+    if (threadIdx.x == 0 && totL) s.baseL = atomicAdd(live_ctr, (unsigned long long)totL);
     __syncthreads();
     if (isL) live_out[s.baseL + exL] = v;
     emit_front_tile(isF, v, d, o, label, a, F, acc, s);
@@ -209,14 +219,48 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     }
     if (Fc == 0) {
       if (remaining == 0) break;
-      // ---- level advance: min alive degree over the live list
+      // ---- level advance: ONE pass over the live list computes the min alive
+      // degree, compacts the list and stages the alive vertices within LW of
+      // the bound; when the new bound lands in that window (the usual case)
+      // the frontier comes from the staged candidates, else a collect pass.
       Acc* acc = a.acc + (f % 3);
       const uint32_t* live_in = lv ? a.live1 : a.live0;
+      uint32_t* live_out = lv ? a.live0 : a.live1;
+      const uint64_t win = bound + LW;
+      if (threadIdx.x == 0) s.cnt = s.lcov = 0;
+      __syncthreads();
       uint32_t lmin = kUnset;
-      for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < livec;
-           i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t v = implicit ? uint32_t(i) : live_in[i];
-        if (a.labels[v] == kUnset) lmin = min(lmin, a.deg[v]);
+      {
+        const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+        for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < livec; base += stride) {
+          const uint64_t i = base + threadIdx.x;
+          uint32_t v = 0, d = kUnset;
+          bool alive = false;
+          if (i < livec) {
+            v = implicit ? uint32_t(i) : live_in[i];
+            alive = a.labels[v] == kUnset;
+            if (alive) d = a.deg[v];
+          }
+          lmin = min(lmin, d);
+          if (alive && d <= win) {
+            const uint32_t slot = atomicAdd(&s.cnt, 1u);
+            if (slot < BUF) {
+              const uint64_t o0 = a.offs[v];
+              s.id[slot] = v;
+              s.rd[slot] = d;
+              s.of[slot] = o0;
+              s.dg[slot] = uint32_t(a.offs[v + 1] - o0);
+            } else {
+              s.lcov = 1;
+            }
+          }
+          uint32_t totL;
+          const uint32_t exL = block_excl_scan<uint32_t>(alive ? 1u : 0u, s.ws32, &totL);
+          if (threadIdx.x == 0 && totL) s.baseL = atomicAdd(&acc->live, (unsigned long long)totL);
+          __syncthreads();
+          if (alive) live_out[s.baseL + exL] = v;
+          __syncthreads();  // s.baseL / ws32 reuse
+        }
       }
       lmin = __reduce_min_sync(~0u, lmin);
       if (lane == 0) s.ws32[threadIdx.x >> 5] = lmin;
@@ -224,7 +268,10 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       if (threadIdx.x < 32) {
         uint32_t x = threadIdx.x < (blockDim.x >> 5) ? s.ws32[threadIdx.x] : kUnset;
         x = __reduce_min_sync(~0u, x);
-        if (threadIdx.x == 0 && x != kUnset) atomicMin(&acc->minv, x);
+        if (threadIdx.x == 0) {
+          if (x != kUnset) atomicMin(&acc->minv, x);
+          if (s.lcov) atomicExch(&acc->cov, 1u);
+        }
       }
       mark(0);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
@@ -247,17 +294,35 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           t = nt;
         }
       }
-      collect(a, livec, implicit, live_in, lv ? a.live0 : a.live1, uint32_t(bound),
-              uint32_t(label), a.fr[f & 1], acc, s);
-      mark(2);
-      if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
-      mark(1);
-      const unsigned long long pk = s.b_front;
-      Fc = uint32_t(pk >> 36);
-      Ftot = pk & M36;
       livec = uint32_t(s.b_live);
       lv ^= 1;
       implicit = false;
+      const Frontier& F0 = a.fr[f & 1];
+      if (!s.b_cov && bound <= win) {
+        // the frontier = staged candidates with residual degree <= bound
+        const uint32_t cnt = min(s.cnt, BUF);
+        for (uint32_t b0 = 0; b0 < cnt; b0 += blockDim.x) {
+          const uint32_t i = b0 + threadIdx.x;
+          const bool ok = i < cnt && s.rd[i] <= bound;
+          emit_front_tile(ok, ok ? s.id[i] : 0, ok ? s.dg[i] : 0, ok ? s.of[i] : 0,
+                          uint32_t(label), a, F0, acc, s);
+        }
+        mark(2);
+        if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
+        mark(1);
+      } else {
+        // larger jump (or a full candidate buffer): collect from the compacted list
+        collect(a, livec, false, live_out, lv ? a.live0 : a.live1, uint32_t(bound),
+                uint32_t(label), F0, acc, s, &acc->live2);
+        mark(2);
+        if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
+        mark(1);
+        livec = uint32_t(s.b_live2);
+        lv ^= 1;
+      }
+      const unsigned long long pk = s.b_front;
+      Fc = uint32_t(pk >> 36);
+      Ftot = pk & M36;
       if (Fc == 0) {
         if (P) a.out[2] = 3;
         break;
@@ -275,6 +340,8 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       r->live = 0;
       r->minv = kUnset;
       r->ovf = 0;
+      r->live2 = 0;
+      r->cov = 0;
     }
     if (threadIdx.x == 0) s.cnt = 0;
     __syncthreads();
@@ -381,7 +448,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     if (s.b_ovf) {
       if (P) ++pr[7];
       collect(a, livec, implicit, lv ? a.live1 : a.live0, lv ? a.live0 : a.live1, uint32_t(bound),
-              uint32_t(label), a.fr[f & 1], nacc, s);
+              uint32_t(label), a.fr[f & 1], nacc, s, &nacc->live);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, nacc); })) break;
       livec = uint32_t(s.b_live);
       lv ^= 1;
@@ -414,6 +481,8 @@ __global__ void k_init_acc(Acc* acc, GridBarrier* bar) {
     acc[threadIdx.x].live = 0;
     acc[threadIdx.x].minv = kUnset;
     acc[threadIdx.x].ovf = 0;
+    acc[threadIdx.x].live2 = 0;
+    acc[threadIdx.x].cov = 0;
   }
   if (threadIdx.x == 0) *bar = GridBarrier{0, 0, 0, 0};
 }
