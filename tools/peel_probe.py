@@ -7,6 +7,8 @@ import paper_2311_04333_b200 as dg  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+if os.environ.get("DG_PEEL_MODE"):  # e.g. 3: candidate-list kernel for every core
+    dg.set_peel_mode(int(os.environ["DG_PEEL_MODE"]))
 u, v = dg.gen_rmat(scale, 16 << scale, scale)
 g = dg.Graph.from_pairs(u, v)
 del u, v
