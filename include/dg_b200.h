@@ -198,6 +198,12 @@ dg_status dg_run(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res
 typedef struct dg_shard dg_shard;
 dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P, uint32_t rank,
                           dg_shard** out);
+/* The same shard from the rank's own rows only (memory-scaled: a rank never
+ * holds the whole graph): offs = the n_local + 1 row offsets of [lo, hi)
+ * (absolute or rebased), adj = their arcs as global dense ids. */
+dg_status dg_shard_create_rows(uint64_t n, const uint64_t* bounds, uint32_t P, uint32_t rank,
+                               const uint64_t* offs, const uint32_t* adj, int on_device,
+                               dg_shard** out);
 void dg_shard_free(dg_shard* s);
 dg_status dg_shard_min_alive(dg_shard* s, uint32_t* min_degree);  /* UINT32_MAX if none */
 dg_status dg_shard_collect(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* nfront);

@@ -75,6 +75,8 @@ PROTOTYPES = {
                          C.POINTER(DgIterRecord), C.c_uint64, u64p, C.c_uint64, u64p,
                          C.c_uint64]),
     "dg_shard_create": (C.c_int, [GP, u64p, C.c_uint32, C.c_uint32, GPP]),
+    "dg_shard_create_rows": (C.c_int, [C.c_uint64, u64p, C.c_uint32, C.c_uint32, u64p, u32p,
+                                       C.c_int, GPP]),
     "dg_shard_free": (None, [GP]),
     "dg_shard_min_alive": (C.c_int, [GP, u32p]),
     "dg_shard_collect": (C.c_int, [GP, C.c_uint32, C.c_uint32, u64p]),

@@ -11,8 +11,10 @@
 #include "internal.cuh"
 
 struct dg_shard {
-  const dg_graph* g = nullptr;  // rows of [lo, hi) are read from this CSR
+  uint64_t n = 0;  // global vertex count
   uint64_t lo = 0, hi = 0;
+  dgb::DevBuf<uint64_t> offs;  // the rank's own rows: local offsets, n_local + 1
+  dgb::DevBuf<uint32_t> adj;   // neighbour ids (global dense ids)
   dgb::DevBuf<uint32_t> deg, labels, front, next;
   dgb::DevBuf<unsigned long long> cnt;  // [0] next size, [1] min, [2..] per-rank counts
   uint64_t nfront = 0;
@@ -25,13 +27,20 @@ namespace {
 
 constexpr uint32_t kUnset = 0xffffffffu;
 
-__global__ void k_sh_init(const uint64_t* offs, uint64_t lo, uint64_t nl, uint32_t* deg,
-                          uint32_t* labels) {
+__global__ void k_sh_init(const uint64_t* offs, uint64_t nl, uint32_t* deg, uint32_t* labels) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nl;
        i += uint64_t(gridDim.x) * blockDim.x) {
-    deg[i] = uint32_t(offs[lo + i + 1] - offs[lo + i]);
+    deg[i] = uint32_t(offs[i + 1] - offs[i]);
     labels[i] = kUnset;
   }
+}
+
+// local offsets of rows [lo, hi) of a global CSR (rebased to 0)
+__global__ void k_sh_rebase(const uint64_t* goffs, uint64_t lo, uint64_t nl, uint64_t* loffs) {
+  const uint64_t b = goffs[lo];
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i <= nl;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    loffs[i] = goffs[lo + i] - b;
 }
 
 __global__ void k_sh_min(const uint32_t* deg, const uint32_t* labels, uint64_t nl,
@@ -82,7 +91,7 @@ __global__ void k_sh_expand(const uint64_t* offs, const uint32_t* adj, uint64_t 
   const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t f = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; f < nfront;
        f += warps) {
-    const uint64_t v = lo + front[f];
+    const uint64_t v = front[f];  // local row
     for (uint64_t p = offs[v] + lane_id(); p < offs[v + 1]; p += 32) {
       const uint64_t u = adj[p];
       if (u >= lo && u < hi) {
@@ -124,16 +133,8 @@ using namespace dgb;
 
 extern "C" {
 
-dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P, uint32_t rank,
-                          dg_shard** out) {
-  SH_TRY
-  if (!g || !bounds || !out || rank >= P) throw DgError(DG_E_PARAM, "bad shard arguments");
-  auto s = std::make_unique<dg_shard>();
-  s->g = g;
-  s->P = P;
-  s->lo = bounds[rank];
-  s->hi = bounds[rank + 1];
-  if (s->lo > s->hi || s->hi > g->n) throw DgError(DG_E_PARAM, "bad shard range");
+// common tail: state arrays, degree init
+static void shard_init_state(dg_shard* s, const uint64_t* bounds, uint32_t P) {
   const uint64_t nl = s->hi - s->lo;
   s->deg.alloc(nl);
   s->labels.alloc(nl);
@@ -143,11 +144,85 @@ dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P,
   s->bounds.alloc(P + 1);
   h2d(s->bounds.get(), bounds, P + 1);
   if (nl) {
-    k_sh_init<<<grid_for(nl, 256), 256, 0, stream()>>>(g->offs.get(), s->lo, nl, s->deg.get(),
+    k_sh_init<<<grid_for(nl, 256), 256, 0, stream()>>>(s->offs.get(), nl, s->deg.get(),
                                                         s->labels.get());
     DG_CHECK_LAUNCH();
   }
   stream_sync();
+}
+
+static void shard_check(uint64_t n, const uint64_t* bounds, uint32_t P, uint32_t rank) {
+  if (!bounds || rank >= P) throw DgError(DG_E_PARAM, "bad shard arguments");
+  if (bounds[0] != 0 || bounds[P] != n) throw DgError(DG_E_PARAM, "bounds must cover [0, n)");
+  for (uint32_t r = 0; r < P; ++r)
+    if (bounds[r] > bounds[r + 1]) throw DgError(DG_E_PARAM, "bounds must ascend");
+}
+
+dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P, uint32_t rank,
+                          dg_shard** out) {
+  SH_TRY
+  if (!g || !out) throw DgError(DG_E_PARAM, "bad shard arguments");
+  shard_check(g->n, bounds, P, rank);
+  auto s = std::make_unique<dg_shard>();
+  s->n = g->n;
+  s->P = P;
+  s->lo = bounds[rank];
+  s->hi = bounds[rank + 1];
+  const uint64_t nl = s->hi - s->lo;
+  // the rank's own rows (the source graph may be freed afterwards)
+  s->offs.alloc(nl + 1);
+  k_sh_rebase<<<grid_for(nl + 1, 256), 256, 0, stream()>>>(g->offs.get(), s->lo, nl,
+                                                            s->offs.get());
+  DG_CHECK_LAUNCH();
+  uint64_t a0 = 0, a1 = 0;
+  d2h(&a0, g->offs.get() + s->lo, 1);
+  d2h(&a1, g->offs.get() + s->hi, 1);
+  stream_sync();
+  s->adj.alloc(a1 - a0);
+  if (a1 > a0)
+    DG_CUDA(cudaMemcpyAsync(s->adj.get(), g->adj.get() + a0, (a1 - a0) * 4,
+                            cudaMemcpyDeviceToDevice, stream()));
+  shard_init_state(s.get(), bounds, P);
+  *out = s.release();
+  SH_END
+}
+
+dg_status dg_shard_create_rows(uint64_t n, const uint64_t* bounds, uint32_t P, uint32_t rank,
+                               const uint64_t* offs, const uint32_t* adj, int on_device,
+                               dg_shard** out) {
+  SH_TRY
+  if (!out || !offs) throw DgError(DG_E_PARAM, "bad shard arguments");
+  shard_check(n, bounds, P, rank);
+  auto s = std::make_unique<dg_shard>();
+  s->n = n;
+  s->P = P;
+  s->lo = bounds[rank];
+  s->hi = bounds[rank + 1];
+  const uint64_t nl = s->hi - s->lo;
+  uint64_t o[2] = {0, 0};
+  if (on_device) {
+    d2h(&o[0], offs, 1);
+    d2h(&o[1], offs + nl, 1);
+    stream_sync();
+  } else {
+    o[0] = offs[0];
+    o[1] = offs[nl];
+  }
+  if (o[1] < o[0]) throw DgError(DG_E_PARAM, "row offsets must ascend");
+  s->offs.alloc(nl + 1);
+  DevBuf<uint64_t> tmp(nl + 1);
+  DG_CUDA(cudaMemcpyAsync(tmp.get(), offs, (nl + 1) * 8,
+                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream()));
+  k_sh_rebase<<<grid_for(nl + 1, 256), 256, 0, stream()>>>(tmp.get(), 0, nl, s->offs.get());
+  DG_CHECK_LAUNCH();
+  s->adj.alloc(o[1] - o[0]);
+  if (o[1] > o[0]) {
+    if (!adj) throw DgError(DG_E_PARAM, "null adjacency");
+    DG_CUDA(cudaMemcpyAsync(s->adj.get(), adj, (o[1] - o[0]) * 4,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            stream()));
+  }
+  shard_init_state(s.get(), bounds, P);
   *out = s.release();
   SH_END
 }
@@ -193,7 +268,7 @@ dg_status dg_shard_count_remote(dg_shard* s, uint64_t* counts) {
   s->cnt.zero();
   if (s->nfront) {
     k_sh_expand<false><<<grid_for(s->nfront * 32, 256), 256, 0, stream()>>>(
-        s->g->offs.get(), s->g->adj.get(), s->lo, s->hi, s->front.get(), s->nfront,
+        s->offs.get(), s->adj.get(), s->lo, s->hi, s->front.get(), s->nfront,
         s->bounds.get(), s->P, s->deg.get(), s->labels.get(), 0, 0, nullptr, s->cnt.get(),
         nullptr, nullptr);
     DG_CHECK_LAUNCH();
@@ -214,7 +289,7 @@ dg_status dg_shard_expand(dg_shard* s, uint32_t bound, uint32_t label, const uin
   s->cnt.zero();
   if (s->nfront) {
     k_sh_expand<true><<<grid_for(s->nfront * 32, 256), 256, 0, stream()>>>(
-        s->g->offs.get(), s->g->adj.get(), s->lo, s->hi, s->front.get(), s->nfront,
+        s->offs.get(), s->adj.get(), s->lo, s->hi, s->front.get(), s->nfront,
         s->bounds.get(), s->P, s->deg.get(), s->labels.get(), bound, label, s->next.get(),
         s->cnt.get(), cur.get(), d_send);
     DG_CHECK_LAUNCH();

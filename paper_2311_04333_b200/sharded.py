@@ -129,7 +129,9 @@ class LocalComm:
 class CudaShard:
     """dg_shard_* over the C ABI; exchange buffers are torch CUDA tensors."""
 
-    def __init__(self, g, bounds: np.ndarray, rank: int):
+    def __init__(self, g, bounds: np.ndarray, rank: int, rows=None):
+        """Shard `rank` of `g` (its rows are copied: `g` may be freed), or --
+        with g=None and rows=(n, offs, adj) -- from the rank's own rows only."""
         import torch
         from . import _chk
         from ._abi import LIB, u32p, u64p
@@ -138,11 +140,23 @@ class CudaShard:
         self.P = len(self.bounds) - 1
         self.rank = rank
         self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
-        self.g = g  # keep the CSR alive
         h = C.c_void_p()
-        _chk(LIB.dg_shard_create(g._h, self.bounds.ctypes.data_as(u64p), self.P, rank,
-                                 C.byref(h)))
+        if rows is None:
+            _chk(LIB.dg_shard_create(g._h, self.bounds.ctypes.data_as(u64p), self.P, rank,
+                                     C.byref(h)))
+        else:
+            n, offs, adj = rows
+            offs = np.ascontiguousarray(offs, dtype=np.uint64)
+            adj = np.ascontiguousarray(adj, dtype=np.uint32)
+            _chk(LIB.dg_shard_create_rows(n, self.bounds.ctypes.data_as(u64p), self.P, rank,
+                                          offs.ctypes.data_as(u64p), adj.ctypes.data_as(u32p), 0,
+                                          C.byref(h)))
         self._h = h
+
+    @classmethod
+    def from_rows(cls, n: int, bounds, rank: int, offs, adj):
+        """Rows [bounds[rank], bounds[rank+1]) only: offs has n_local + 1 entries."""
+        return cls(None, bounds, rank, rows=(n, offs, adj))
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -140,3 +140,30 @@ def test_cuda_shards_rmat16(orc, dg):
     np.testing.assert_array_equal(dec.labels, one.labels)
     assert (dec.kmax, dec.peel_rounds) == (one.kmax, one.peel_rounds)
     _check(orc, hg, [dec.labels], dec.kmax, dec.peel_rounds, None)
+
+
+@pytest.mark.gpu
+def test_cuda_shards_from_own_rows(orc, dg):
+    """Memory-scaled shards: each is created from its own rows only (host
+    slices of the CSR), or copies its rows from a graph that is then freed."""
+    from paper_2311_04333_b200.sharded import CudaShard, LocalComm
+    u, v = orc.gen_rmat(14, 16 << 14, 77)
+    hg = orc.build(u, v)
+    lab, kmax, rounds = orc.coreness(hg)
+    for P in (1, 3, 5):
+        b = partition(hg.offs, P)
+        shards = []
+        for r in range(P):
+            lo, hi = int(b[r]), int(b[r + 1])
+            offs = hg.offs[lo:hi + 1]
+            adj = hg.adj[int(offs[0]):int(offs[-1])]
+            shards.append(CudaShard.from_rows(hg.n, b, r, offs, adj))
+        labs, k, rr = sharded_coreness(shards, LocalComm(P), hg.n)
+        np.testing.assert_array_equal(np.concatenate(labs), lab)
+        assert (k, rr) == (kmax, rounds)
+    g = dg.Graph.from_csr(hg.offs, hg.adj, hg.orig)
+    b = partition(hg.offs, 4)
+    shards = [CudaShard(g, b, r) for r in range(4)]
+    del g  # shards own their rows
+    labs, k, rr = sharded_coreness(shards, LocalComm(4), hg.n)
+    np.testing.assert_array_equal(np.concatenate(labs), lab)
