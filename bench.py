@@ -332,13 +332,17 @@ def run_ours(args, cfg, rank, world, local):
     p_orig, _t3 = pinned_copy(orig)
     e2e_edges = e2e_s = 0.0
     d2h = 0
+    e2e_steps = []
     for _ in range(max(1, min(args.steps, 5))):
         dg.flush_l2()
+        dg.synchronize()
         t0 = time.perf_counter()
         g2 = dg.Graph.from_csr(p_offs, p_adj, p_orig)
         r = dg.run(g2, rcfg)
         del g2
-        e2e_s += time.perf_counter() - t0
+        dt = time.perf_counter() - t0
+        e2e_steps.append(round(1e3 * dt, 2))
+        e2e_s += dt
         e2e_edges += sum(it.m for it in r.trace.iters)
         d2h = 8 * (len(r.witness) + len(r.trace.final_vertices)) + 80 * len(r.trace.iters) + 64
     e2e_s = allreduce([e2e_s], "max", world, local)[0]
@@ -346,6 +350,7 @@ def run_ours(args, cfg, rank, world, local):
     line["e2e"] = {"value": e2e_edges / e2e_s, "unit": "edges/s",
                    "h2d_bytes_per_step": int(p_offs.nbytes + p_adj.nbytes + p_orig.nbytes),
                    "d2h_bytes_per_step": int(d2h),
+                   "step_ms": e2e_steps,
                    "includes": "H2D CSR + k-core + prune + T iterations + witness recount + D2H"}
 
     # ---- CPU baseline: the reference library on this host (rank 0, N=1)
