@@ -46,6 +46,9 @@ CONFIGS = {
     "rmat26": dict(kind="rmat", scale=26, edge_factor=16, seed=26, T=10, eps=0.1),
     # configs[2]: Chung-Lu n=50M, 500M endpoint pairs, exponent 2.1, T=20
     "chunglu50m": dict(kind="cl", n=50_000_000, pairs=500_000_000, seed=50, T=20, eps=0.05),
+    # configs[4]: RMAT-28 (4.3e9 samples), T=5 -- listed for 2-8 GPUs; fits one
+    # B200 through the streamed build
+    "rmat28": dict(kind="rmat", scale=28, edge_factor=16, seed=28, T=5, eps=0.1),
     # small config for quick checks / profiling
     "rmat18": dict(kind="rmat", scale=18, edge_factor=16, seed=18, T=20, eps=0.05),
 }
@@ -159,24 +162,14 @@ def host_pairs(cfg):
 
 
 def device_graph(dg, cfg):
-    """Generate the seeded pairs on the device and build the CSR there."""
+    """The seeded graph built on the device straight from the generator
+    (dg_graph_generate: no pair arrays, source-range parts)."""
     if cfg["kind"] == "er":
         u, v = host_pairs(cfg)
         return dg.Graph.from_pairs(u, v)
-    import ctypes as C
-    k = cfg["edge_factor"] << cfg["scale"] if cfg["kind"] == "rmat" else cfg["pairs"]
-    bu, bv = dg.DeviceBuffer(8 * k), dg.DeviceBuffer(8 * k)
     if cfg["kind"] == "rmat":
-        dg._chk(dg.LIB.dg_gen_rmat(cfg["scale"], k, cfg["seed"], C.c_void_p(bu.ptr),
-                                   C.c_void_p(bv.ptr), 1))
-    else:
-        R = float(cfg["n"]) ** (1.0 / 11.0)
-        dg._chk(dg.LIB.dg_gen_chung_lu(cfg["n"], k, R, cfg["seed"], C.c_void_p(bu.ptr),
-                                       C.c_void_p(bv.ptr), 1))
-    g = dg.Graph.from_device_pairs(bu.ptr, bv.ptr, k)
-    bu.free()
-    bv.free()
-    return g
+        return dg.Graph.generate_rmat(cfg["scale"], cfg["edge_factor"] << cfg["scale"], cfg["seed"])
+    return dg.Graph.generate_chung_lu(cfg["n"], cfg["pairs"], cfg["seed"])
 
 
 def pinned_copy(a):

@@ -61,6 +61,14 @@ dg_status dg_graph_build(const uint64_t* u, const uint64_t* v, uint64_t k, int o
 
 /* Wrap an existing CSR (Graph{n,m,offs,adj,orig}, graph.hpp:24-30). Copies
  * host arrays (on_device == 0) or device arrays (on_device != 0). */
+/* The CSR of a seeded synthetic graph built straight from the device
+ * generator (no pair arrays; source-range parts so the largest BASELINE
+ * configuration, RMAT-28, builds on one GPU).  Identical to dg_graph_build on
+ * the pairs of dg_gen_rmat / dg_gen_chung_lu.  kind 0: RMAT (size = scale),
+ * 1: Chung-Lu (size = n, root = n^(1/11)); part_cap = max arc emissions per
+ * part (0: from free memory). */
+dg_status dg_graph_generate(int kind, uint64_t size, uint64_t samples, uint64_t seed,
+                            double root, uint64_t part_cap, dg_graph** out);
 /* parse_edge_list(istream&, ParseOptions) (io.hpp:18-19, io.cpp:25-94): edge-
  * list text (len bytes, host or device memory) tokenised ON THE DEVICE with
  * the reference's rules, then the CSR build of dg_graph_build.  Malformed

@@ -207,6 +207,22 @@ class Graph:
         return cls(h)
 
     @classmethod
+    def generate_rmat(cls, scale: int, samples: int, seed: int, part_cap: int = 0) -> "Graph":
+        """The CSR of gen_rmat's pairs, built from the device generator without the
+        pair arrays (source-range parts; RMAT-28 fits one GPU)."""
+        h = C.c_void_p()
+        _chk(LIB.dg_graph_generate(0, scale, samples, seed, 0.0, part_cap, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def generate_chung_lu(cls, n: int, pairs: int, seed: int, part_cap: int = 0) -> "Graph":
+        """The CSR of gen_chung_lu's pairs, built from the device generator."""
+        h = C.c_void_p()
+        R = float(n) ** (1.0 / 11.0)
+        _chk(LIB.dg_graph_generate(1, n, pairs, seed, R, part_cap, C.byref(h)))
+        return cls(h)
+
+    @classmethod
     def from_csr(cls, offs, adj, orig) -> "Graph":
         offs = np.ascontiguousarray(offs, dtype=np.uint64)
         adj = np.ascontiguousarray(adj, dtype=np.uint32)

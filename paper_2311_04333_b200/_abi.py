@@ -54,6 +54,8 @@ PROTOTYPES = {
     "dg_last_error": (C.c_char_p, []),
     "dg_version": (C.c_char_p, []),
     "dg_graph_build": (C.c_int, [u64p, u64p, C.c_uint64, C.c_int, GPP]),
+    "dg_graph_generate": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
+                                    C.c_uint64, GPP]),
     "dg_parse_edge_list": (C.c_int, [C.c_char_p, C.c_uint64, C.c_char, C.c_int, GPP, u64p]),
     "dg_graph_from_csr": (C.c_int, [C.c_uint64, u64p, u32p, u64p, C.c_int, GPP]),
     "dg_graph_info": (C.c_int, [GP, u64p, u64p, u64p]),

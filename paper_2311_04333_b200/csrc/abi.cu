@@ -419,6 +419,23 @@ dg_status dg_graph_build(const uint64_t* u, const uint64_t* v, uint64_t k, int o
   DG_API_END
 }
 
+dg_status dg_graph_generate(int kind, uint64_t size, uint64_t samples, uint64_t seed,
+                            double root, uint64_t part_cap, dg_graph** out) {
+  DG_API_BEGIN
+  if (!out) throw DgError(DG_E_PARAM, "null output");
+  *out = nullptr;
+  GraphPtr g;
+  if (kind == 0)
+    g = build_rmat_streamed(uint32_t(size), samples, seed, part_cap);
+  else if (kind == 1)
+    g = build_chung_lu_streamed(size, samples, root, seed, part_cap);
+  else
+    throw DgError(DG_E_PARAM, "unknown generator kind");
+  stream_sync();
+  *out = g.release();
+  DG_API_END
+}
+
 dg_status dg_parse_edge_list(const char* text, uint64_t len, char comment, int on_device,
                              dg_graph** out, uint64_t* bad_line) {
   DG_API_BEGIN

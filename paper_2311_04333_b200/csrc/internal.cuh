@@ -20,6 +20,10 @@ using GraphPtr = std::unique_ptr<dg_graph>;
 
 // ---- graph.cu ----
 GraphPtr build_from_pairs(const uint64_t* d_u, const uint64_t* d_v, uint64_t k);
+// graph_stream.cu: CSR straight from a device generator, in source-range parts
+GraphPtr build_rmat_streamed(uint32_t scale, uint64_t samples, uint64_t seed, uint64_t part_cap);
+GraphPtr build_chung_lu_streamed(uint64_t n, uint64_t pairs, double R, uint64_t seed,
+                                 uint64_t part_cap);
 // parse.cu: edge-list text on the device -> CSR (DG_E_PARSE sets *bad_line)
 GraphPtr parse_edge_list(const uint8_t* d_text, uint64_t len, uint8_t comment, uint64_t* bad_line);
 GraphPtr graph_from_device_csr(uint64_t n, const uint64_t* d_offs, const uint32_t* d_adj,

@@ -465,3 +465,24 @@ def test_parse_edge_list_at_scale(dg, orc, tmp_path):
     assert (sha(g2.offs), sha(g2.adj)) == (sha(g.offs), sha(g.adj))
     with pytest.raises(dg.IoError):
         dg.parse_edge_list_file(str(tmp_path / "missing.txt"))
+
+
+def test_streamed_generator_build(dg, orc):
+    """dg_graph_generate (CSR straight from the device generator, in
+    source-range parts) equals the pair-based build of the same samples,
+    with one part and with many tiny parts."""
+    for scale, cap in ((14, 0), (14, 5000), (17, 0), (17, 200000)):
+        u, v = dg.gen_rmat(scale, 16 << scale, 3 * scale)
+        ref = dg.Graph.from_pairs(u, v)
+        g = dg.Graph.generate_rmat(scale, 16 << scale, 3 * scale, cap)
+        assert (g.n, g.m) == (ref.n, ref.m)
+        assert (sha(g.offs), sha(g.adj), sha(g.orig)) == (sha(ref.offs), sha(ref.adj), sha(ref.orig))
+    for n, pairs, cap in ((20000, 200000, 0), (20000, 200000, 7000)):
+        u, v = dg.gen_chung_lu(n, pairs, 5)
+        ref = dg.Graph.from_pairs(u, v)
+        g = dg.Graph.generate_chung_lu(n, pairs, 5, cap)
+        assert (sha(g.offs), sha(g.adj), sha(g.orig)) == (sha(ref.offs), sha(ref.adj), sha(ref.orig))
+    with pytest.raises(dg.ParamError):
+        dg.Graph.generate_rmat(0, 10, 1)
+    with pytest.raises(dg.EmptyGraphError):
+        dg.Graph.generate_rmat(1, 0, 1)
