@@ -321,8 +321,8 @@ bool launch_queue(const dg_graph& g, const uint64_t* d_loads, uint64_t base, uin
   switch (vq) {
 #define DG_VQ(V)                                                                        \
   case V:                                                                               \
-    return OFFS && peel_trace_armed()                                                   \
-               ? launch_queue1<OFFS, V, OFFS>(g, d_loads, base, d_perm, d_raw, d_batches) \
+    return peel_trace_armed()                                                           \
+               ? launch_queue1<OFFS, V, true>(g, d_loads, base, d_perm, d_raw, d_batches) \
                : launch_queue1<OFFS, V>(g, d_loads, base, d_perm, d_raw, d_batches);
     DG_VQ(1) DG_VQ(3) DG_VQ(5) DG_VQ(7) DG_VQ(9)
 #undef DG_VQ

@@ -40,7 +40,6 @@ using peelk::Range;
 constexpr int PT = 1024;
 constexpr uint32_t NW = PT / 32;
 constexpr int UQ = 2;              // adjacency quads in flight per thread
-constexpr int U = 4;               // arcs in flight per thread (slice path)
 constexpr uint32_t LCAP = 4096;    // candidate list capacity
 constexpr uint32_t LPT = LCAP / PT;
 #ifndef DG_PEEL_LTARGET
@@ -154,47 +153,58 @@ __device__ __forceinline__ void remove_row(const uint4* adj4, uint32_t keys_s, u
   }
 }
 
-// removal of staged members [0, sl) with a CTA scan over their degrees;
-// every thread calls it (barriers inside)
+// removal of staged members [0, sl) -- every thread calls it (barriers
+// inside).  The members' rows are concatenated as 16-byte quads (a CTA scan
+// over per-member quad counts); warps take 32-quad chunks, a lane finds its
+// member by stepping forward from the chunk's first member (rows are long,
+// so usually zero steps), loads its quad and decrements its valid arcs.
 __device__ __forceinline__ void remove_slice(const uint32_t* adj, uint32_t keys_s, uint32_t sl,
                                              uint32_t tid, uint32_t lane, uint32_t w,
                                              uint32_t thr, Q& q, uint32_t buf) {
-  const uint64_t d = tid < sl ? q.mdeg[tid] : 0;
+  const uint4* adj4 = reinterpret_cast<const uint4*>(adj);
+  const uint64_t nqj =
+      tid < sl ? ((q.moff[tid] & 3) + q.mdeg[tid] + 3) >> 2 : 0;  // quads of member tid
   uint64_t tot;
-  const uint64_t ex = block_excl_scan(d, q.ws, &tot);
-  q.pre[tid] = ex + d;
+  const uint64_t ex = block_excl_scan(nqj, q.ws, &tot);
+  q.pre[tid] = ex;  // first quad of member tid (exclusive prefix)
   __syncthreads();
-  for (uint64_t b0 = uint64_t(w) * 32 * U; b0 < tot; b0 += uint64_t(PT) * U) {
-    uint32_t u[U], bb[U];
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const uint64_t x = b0 + uint64_t(j) * 32 + lane;
-      u[j] = 0xffffffffu;
-      bb[j] = 0;
-      if (x < tot) {
-        uint32_t l = 0, h = sl - 1;
-        while (l < h) {
-          const uint32_t mid = (l + h) >> 1;
-          if (q.pre[mid] > x)
-            h = mid;
-          else
-            l = mid + 1;
-        }
-        bb[j] = l;
-        u[j] = adj[q.moff[l] + (x - (l ? q.pre[l - 1] : 0))];
+  const uint64_t nch = (tot + 31) / 32;
+  for (uint64_t c = w; c < nch; c += NW) {
+    const uint64_t x0 = c * 32;
+    // chunk's first member: largest j with pre[j] <= x0 (lane-parallel search)
+    uint32_t j0 = 0;
+    {
+      uint32_t lo = 0, hi = sl - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (q.pre[mid] <= x0)
+          lo = mid;
+        else
+          hi = mid - 1;
       }
+      j0 = lo;
     }
-    uint32_t old[U];
+    const uint64_t x = x0 + lane;
+    if (x >= tot) continue;
+    uint32_t j = j0;
+    while (j + 1 < sl && q.pre[j + 1] <= x) ++j;
+    const uint64_t oj = q.moff[j];
+    const uint32_t head = uint32_t(oj & 3), end = head + q.mdeg[j];
+    const uint32_t qi = uint32_t(x - q.pre[j]);
+    const uint4 v4 = __ldg(adj4 + (oj >> 2) + qi);
+    const uint32_t us[4] = {v4.x, v4.y, v4.z, v4.w};
+    const uint32_t vj = q.mem[j];
+    uint32_t old[4];
+    const uint32_t e0 = qi << 2;
 #pragma unroll
-    for (int j = 0; j < U; ++j) old[j] = u[j] != 0xffffffffu ? dec_atom(keys_s, u[j]) : 0u;
+    for (int e = 0; e < 4; ++e)
+      old[e] = (e0 + e >= head && e0 + e < end) ? dec_atom(keys_s, us[e]) : R::DEAD;
 #pragma unroll
-    for (int j = 0; j < U; ++j)
-      if (u[j] != 0xffffffffu)
-        dec_check<false>(old[j], u[j], q.mem[bb[j]], &q.mcnt[bb[j]], thr, q, buf);
+    for (int e = 0; e < 4; ++e)
+      if (e0 + e >= head && e0 + e < end) dec_check<false>(old[e], us[e], vj, &q.mcnt[j], thr, q, buf);
   }
 }
 
-// TR: timeline variant (dg_peel_trace_*; stamps as in peel_kernel.cuh)
 template <bool OFFS, int VQ, bool TR>
 __global__ void __launch_bounds__(PT, 1) k_peel_queue(Args a) {
   extern __shared__ __align__(16) unsigned char raw_smem[];

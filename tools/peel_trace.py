@@ -24,7 +24,8 @@ del u, v
 mode = int(sys.argv[3], 0) if len(sys.argv) > 3 else 0
 dg.set_peel_mode(mode)
 dg._chk(dg.LIB.dg_peel_trace_arm(first))
-r = dg.run(g, dg.RunConfig(iterations=3))
+T = int(os.environ.get("DG_TRACE_T", "3"))  # 1: iteration 1's core
+r = dg.run(g, dg.RunConfig(iterations=T))
 tr = np.zeros(8 * 32 * 12, np.uint64)
 dg._chk(dg.LIB.dg_peel_trace_read(tr.ctypes.data_as(C.POINTER(C.c_uint64))))
 dg._chk(dg.LIB.dg_peel_trace_arm(0xFFFFFFFF))  # disarm
