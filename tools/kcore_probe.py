@@ -9,9 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2311_04333_b200 as dg  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
-u, v = dg.gen_rmat(scale, 16 << scale, scale)
-g = dg.Graph.from_pairs(u, v)
-del u, v
+g = dg.Graph.generate_rmat(scale, 16 << scale, scale)
 for _ in range(2):
     r = dg.run(g, dg.RunConfig(iterations=1))
 p = np.zeros(8 + 3 * 4096, np.uint64)
