@@ -47,7 +47,7 @@ struct alignas(128) Acc {  // one cache line each: no false sharing between phas
   uint32_t minv;             // min alive degree (level advance)
   uint32_t ovf;              // some CTA buffer overflowed while building
   unsigned long long live2;  // live-list entries of a fallback collect (level advance)
-  uint32_t cov;              // a CTA's level-advance candidate buffer overflowed
+  unsigned long long ccnt;   // level-advance candidates spilled to KcArgs::cand
 };
 
 struct Frontier {
@@ -65,6 +65,7 @@ struct KcArgs {
   uint32_t* labels;
   uint32_t* live0;
   uint32_t* live1;
+  uint32_t* cand;  // level-advance candidates spilled by full CTA buffers (capacity n)
   Frontier fr[2];
   Acc* acc;  // [3]
   GridBarrier* bar;
@@ -87,13 +88,13 @@ struct Smem {
   unsigned long long baseF, baseL;
   // phase scalars fetched by thread 0 after each grid barrier
   uint32_t abort;
-  unsigned long long b_front, b_live, b_live2;
-  uint32_t b_minv, b_ovf, b_cov;
-  uint32_t lcov;  // this CTA's candidate buffer overflowed (level advance)
+  unsigned long long b_front, b_live, b_live2, b_ccnt;
+  uint32_t b_minv, b_ovf;
 };
 
 // Level advance candidates: alive vertices within LW of the current bound are
-// staged during the min scan, so the usual small jump needs no second pass.
+// staged in shared memory during the min scan (a CTA's overflow spills to a
+// global list), so the usual small jump needs no second pass.
 constexpr uint32_t LW = 16;
 
 __device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
@@ -102,7 +103,7 @@ __device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
   s.b_minv = ld_relaxed_u32(&acc->minv);
   s.b_ovf = ld_relaxed_u32(&acc->ovf);
   s.b_live2 = ld_relaxed_u64(&acc->live2);
-  s.b_cov = ld_relaxed_u32(&acc->cov);
+  s.b_ccnt = ld_relaxed_u64(&acc->ccnt);
 }
 
 // All threads of the CTA call this with a per-thread candidate (isF, v, d, o).
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       const uint32_t* live_in = lv ? a.live1 : a.live0;
       uint32_t* live_out = lv ? a.live0 : a.live1;
       const uint64_t win = bound + LW;
-      if (threadIdx.x == 0) s.cnt = s.lcov = 0;
+      if (threadIdx.x == 0) s.cnt = 0;
       __syncthreads();
       uint32_t lmin = kUnset;
       {
@@ -242,6 +243,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
             if (alive) d = a.deg[v];
           }
           lmin = min(lmin, d);
+          bool spill = false;
           if (alive && d <= win) {
             const uint32_t slot = atomicAdd(&s.cnt, 1u);
             if (slot < BUF) {
@@ -251,7 +253,16 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
               s.of[slot] = o0;
               s.dg[slot] = uint32_t(a.offs[v + 1] - o0);
             } else {
-              s.lcov = 1;
+              spill = true;
+            }
+          }
+          {  // overflow -> global candidate list, warp-aggregated
+            const uint32_t cm = __ballot_sync(~0u, spill);
+            if (cm) {
+              unsigned long long cb = 0;
+              if (lane == 0) cb = atomicAdd(&acc->ccnt, (unsigned long long)__popc(cm));
+              cb = __shfl_sync(~0u, cb, 0);
+              if (spill) a.cand[cb + __popc(cm & ((1u << lane) - 1u))] = v;
             }
           }
           uint32_t totL;
@@ -268,10 +279,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       if (threadIdx.x < 32) {
         uint32_t x = threadIdx.x < (blockDim.x >> 5) ? s.ws32[threadIdx.x] : kUnset;
         x = __reduce_min_sync(~0u, x);
-        if (threadIdx.x == 0) {
-          if (x != kUnset) atomicMin(&acc->minv, x);
-          if (s.lcov) atomicExch(&acc->cov, 1u);
-        }
+        if (threadIdx.x == 0 && x != kUnset) atomicMin(&acc->minv, x);
       }
       mark(0);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
@@ -298,8 +306,9 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       lv ^= 1;
       implicit = false;
       const Frontier& F0 = a.fr[f & 1];
-      if (!s.b_cov && bound <= win) {
-        // the frontier = staged candidates with residual degree <= bound
+      if (bound <= win) {
+        // the frontier = candidates with residual degree <= bound: this CTA's
+        // staged ones, then a grid-strided share of the spilled ones
         const uint32_t cnt = min(s.cnt, BUF);
         for (uint32_t b0 = 0; b0 < cnt; b0 += blockDim.x) {
           const uint32_t i = b0 + threadIdx.x;
@@ -307,11 +316,28 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           emit_front_tile(ok, ok ? s.id[i] : 0, ok ? s.dg[i] : 0, ok ? s.of[i] : 0,
                           uint32_t(label), a, F0, acc, s);
         }
+        const uint64_t cc = s.b_ccnt;
+        for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < cc;
+             base += uint64_t(gridDim.x) * blockDim.x) {
+          const uint64_t i = base + threadIdx.x;
+          bool ok = false;
+          uint32_t v = 0, dl = 0;
+          uint64_t o = 0;
+          if (i < cc) {
+            v = a.cand[i];
+            if (a.deg[v] <= bound) {
+              ok = true;
+              o = a.offs[v];
+              dl = uint32_t(a.offs[v + 1] - o);
+            }
+          }
+          emit_front_tile(ok, v, dl, o, uint32_t(label), a, F0, acc, s);
+        }
         mark(2);
         if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
         mark(1);
       } else {
-        // larger jump (or a full candidate buffer): collect from the compacted list
+        // larger jump: collect from the compacted list
         collect(a, livec, false, live_out, lv ? a.live0 : a.live1, uint32_t(bound),
                 uint32_t(label), F0, acc, s, &acc->live2);
         mark(2);
@@ -341,7 +367,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       r->minv = kUnset;
       r->ovf = 0;
       r->live2 = 0;
-      r->cov = 0;
+      r->ccnt = 0;
     }
     if (threadIdx.x == 0) s.cnt = 0;
     __syncthreads();
@@ -482,7 +508,7 @@ __global__ void k_init_acc(Acc* acc, GridBarrier* bar) {
     acc[threadIdx.x].minv = kUnset;
     acc[threadIdx.x].ovf = 0;
     acc[threadIdx.x].live2 = 0;
-    acc[threadIdx.x].cov = 0;
+    acc[threadIdx.x].ccnt = 0;
   }
   if (threadIdx.x == 0) *bar = GridBarrier{0, 0, 0, 0};
 }
@@ -513,7 +539,7 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   if (g.n >= (1ULL << 28) || 2 * g.m >= (1ULL << 36))
     throw DgError(DG_E_PARAM, "graph too large for the single-GPU coreness kernel");
   const uint64_t n = g.n;
-  DevBuf<uint32_t> deg(n), live0(n), live1(n), v0(n), v1(n);
+  DevBuf<uint32_t> deg(n), live0(n), live1(n), v0(n), v1(n), cand(n);
   DevBuf<uint64_t> fa0(n), fa1(n), fo0(n), fo1(n);
   const uint64_t nch = (2 * g.m) / CH + 2;
   DevBuf<uint32_t> cse0(nch), cse1(nch);
@@ -541,6 +567,7 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
               d_labels,
               live0.get(),
               live1.get(),
+              cand.get(),
               {Frontier{v0.get(), fa0.get(), fo0.get(), cse0.get()},
                Frontier{v1.get(), fa1.get(), fo1.get(), cse1.get()}},
               acc.get(),
