@@ -28,6 +28,8 @@
 //   * one grid barrier per round (two per level advance); only thread 0 of a
 //     CTA touches the barrier and the phase scalars (fetched into shared
 //     memory), so no L2 line is hammered by the whole grid.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace dgb {
@@ -66,6 +68,7 @@ struct KcArgs {
   uint32_t* live0;
   uint32_t* live1;
   uint32_t* cand;  // level-advance candidates spilled by full CTA buffers (capacity n)
+  uint32_t* alive;  // alive bitmap (n bits; large graphs only, see k_coreness<BM>)
   Frontier fr[2];
   Acc* acc;  // [3]
   GridBarrier* bar;
@@ -126,6 +129,7 @@ __device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d
     F.fa[e0 + k] = A;
     F.fo[e0 + k] = o;
     a.labels[v] = label;
+    if (a.alive) atomicAnd(&a.alive[v >> 5], ~(1u << (v & 31)));
     s.tileA[k] = A;
   }
   __syncthreads();
@@ -185,6 +189,9 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t x, uint32_t src) {
   return __shfl_sync(~0u, x, src);
 }
 
+// BM: graphs whose degree array exceeds L2 first test an L2-resident alive
+// bitmap, so arcs to removed vertices skip the random HBM read of deg.
+template <bool BM>
 __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -434,7 +441,11 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
         for (int k = 0; k < UC; ++k) {
           const uint32_t uv = u[k];
           if (uv == kUnset) continue;
-          if (a.deg[uv] <= b32) continue;  // dead, or already at/below the bound
+          if (BM) {
+            if (!((ld_relaxed_u32(&a.alive[uv >> 5]) >> (uv & 31)) & 1u)) continue;  // removed
+          } else if (a.deg[uv] <= b32) {
+            continue;  // dead, or already at/below the bound
+          }
           const uint32_t old = atomicSub(&a.deg[uv], 1u);
           if (old == b32 + 1) {  // crossed: joins the next round
             const uint32_t slot = atomicAdd(&s.cnt, 1u);
@@ -540,6 +551,15 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
     throw DgError(DG_E_PARAM, "graph too large for the single-GPU coreness kernel");
   const uint64_t n = g.n;
   DevBuf<uint32_t> deg(n), live0(n), live1(n), v0(n), v1(n), cand(n);
+  // alive bitmap when the degree array does not stay in L2 (~126 MB);
+  // DG_KCORE_BITMAP=0/1 overrides (tests, tuning)
+  bool bm = n * 4 > (48ULL << 20);
+  if (const char* e = getenv("DG_KCORE_BITMAP")) bm = e[0] == '1';
+  DevBuf<uint32_t> alive;
+  if (bm) {
+    alive.alloc((n + 31) / 32);
+    DG_CUDA(cudaMemsetAsync(alive.get(), 0xff, ((n + 31) / 32) * 4, stream()));
+  }
   DevBuf<uint64_t> fa0(n), fa1(n), fo0(n), fo1(n);
   const uint64_t nch = (2 * g.m) / CH + 2;
   DevBuf<uint32_t> cse0(nch), cse1(nch);
@@ -553,10 +573,10 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   DG_CHECK_LAUNCH();
 
   const size_t smem = sizeof(Smem);
-  DG_CUDA(cudaFuncSetAttribute(k_coreness, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
+  void* kfn = bm ? (void*)k_coreness<true> : (void*)k_coreness<false>;
+  DG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int occ = 0;
-  DG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coreness, KC_THREADS, smem));
+  DG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, KC_THREADS, smem));
   if (occ < 1) throw DgError(DG_E_CUDA, "coreness kernel does not fit on an SM");
   const unsigned blocks = unsigned(num_sms());  // one persistent CTA per SM
 
@@ -568,6 +588,7 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
               live0.get(),
               live1.get(),
               cand.get(),
+              bm ? alive.get() : nullptr,
               {Frontier{v0.get(), fa0.get(), fo0.get(), cse0.get()},
                Frontier{v1.get(), fa1.get(), fo1.get(), cse1.get()}},
               acc.get(),
@@ -583,7 +604,7 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   DG_CUDA(cudaEventCreate(&e0));
   DG_CUDA(cudaEventCreate(&e1));
   DG_CUDA(cudaEventRecord(e0, stream()));
-  DG_CUDA(cudaLaunchCooperativeKernel((void*)k_coreness, dim3(blocks), dim3(KC_THREADS), params,
+  DG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(KC_THREADS), params,
                                       smem, stream()));
   count_launch();
   DG_CUDA(cudaEventRecord(e1, stream()));

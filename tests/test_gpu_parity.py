@@ -9,6 +9,7 @@ import hashlib
 import json
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -486,3 +487,31 @@ def test_streamed_generator_build(dg, orc):
         dg.Graph.generate_rmat(0, 10, 1)
     with pytest.raises(dg.EmptyGraphError):
         dg.Graph.generate_rmat(1, 0, 1)
+
+
+def test_coreness_alive_bitmap_variant(orc):
+    """The k-core kernel's alive-bitmap variant (chosen for graphs whose degree
+    array exceeds L2) forced on a medium graph: labels, kmax, peel_rounds
+    (exact and approximate) against the oracle."""
+    code = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "oracle"))
+import paper_2311_04333_b200 as dg
+from oracle import Oracle
+orc = Oracle()
+u, v = orc.gen_rmat(17, 16 << 17, 99)
+h = orc.build(u, v)
+g = dg.Graph.from_pairs(u, v)
+d = dg.exact_coreness(g)
+lab, kmax, rounds = orc.coreness(h)
+assert np.array_equal(d.labels, lab) and (d.kmax, d.peel_rounds) == (kmax, rounds)
+a = dg.approx_coreness(g, 3, 2)
+al, ak, ar = orc.coreness(h, True, 3, 2)
+assert np.array_equal(a.labels, al) and (a.kmax, a.peel_rounds) == (ak, ar)
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DG_KCORE_BITMAP="1", ROOT=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
