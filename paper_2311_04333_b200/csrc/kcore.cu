@@ -154,6 +154,7 @@ __device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d
 
 // Scan the live list: alive vertices with deg <= bound join the frontier,
 // the other alive ones are compacted into live_out.
+template <bool BM>
 __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const uint32_t* live_in,
                         uint32_t* live_out, uint32_t bound, uint32_t label, const Frontier& F,
                         Acc* acc, Smem& s, unsigned long long* live_ctr) {
@@ -165,7 +166,8 @@ __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const ui
     bool isF = false, isL = false;
     if (i < livec) {
       v = implicit ? uint32_t(i) : live_in[i];
-      if (a.labels[v] == kUnset) {
+      if (BM ? ((ld_relaxed_u32(&a.alive[v >> 5]) >> (v & 31)) & 1u) != 0
+             : a.labels[v] == kUnset) {
         if (a.deg[v] <= bound) {
           isF = true;
           o = a.offs[v];
@@ -246,7 +248,8 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           bool alive = false;
           if (i < livec) {
             v = implicit ? uint32_t(i) : live_in[i];
-            alive = a.labels[v] == kUnset;
+            alive = BM ? ((ld_relaxed_u32(&a.alive[v >> 5]) >> (v & 31)) & 1u) != 0
+                       : a.labels[v] == kUnset;
             if (alive) d = a.deg[v];
           }
           lmin = min(lmin, d);
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
         mark(1);
       } else {
         // larger jump: collect from the compacted list
-        collect(a, livec, false, live_out, lv ? a.live0 : a.live1, uint32_t(bound),
+        collect<BM>(a, livec, false, live_out, lv ? a.live0 : a.live1, uint32_t(bound),
                 uint32_t(label), F0, acc, s, &acc->live2);
         mark(2);
         if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
@@ -484,7 +487,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     ++f;
     if (s.b_ovf) {
       if (P) ++pr[7];
-      collect(a, livec, implicit, lv ? a.live1 : a.live0, lv ? a.live0 : a.live1, uint32_t(bound),
+      collect<BM>(a, livec, implicit, lv ? a.live1 : a.live0, lv ? a.live0 : a.live1, uint32_t(bound),
               uint32_t(label), a.fr[f & 1], nacc, s, &nacc->live);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, nacc); })) break;
       livec = uint32_t(s.b_live);
