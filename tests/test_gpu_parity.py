@@ -489,9 +489,9 @@ def test_streamed_generator_build(dg, orc):
         dg.Graph.generate_rmat(1, 0, 1)
 
 
-def test_coreness_alive_bitmap_variant(orc):
-    """The k-core kernel's alive-bitmap variant (chosen for graphs whose degree
-    array exceeds L2) forced on a medium graph: labels, kmax, peel_rounds
+def test_coreness_without_alive_bitmap(orc):
+    """The k-core kernel's variant without the alive bitmap (DG_KCORE_BITMAP=0;
+    the bitmap is the default) on a medium graph: labels, kmax, peel_rounds
     (exact and approximate) against the oracle."""
     code = r"""
 import os, sys, numpy as np
@@ -511,7 +511,7 @@ assert np.array_equal(a.labels, al) and (a.kmax, a.peel_rounds) == (ak, ar)
 print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DG_KCORE_BITMAP="1", ROOT=root)
+    env = dict(os.environ, DG_KCORE_BITMAP="0", ROOT=root)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
