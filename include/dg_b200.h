@@ -266,7 +266,8 @@ dg_status dg_peel_profile(uint64_t out[16]);
  * and record a per-warp timeline (SM cycles) of batches [first_batch,
  * first_batch + 8) of subsequent launches; 0xFFFFFFFF disarms.  Read it as
  * [8 batches][32 warps][12 stamps]: loop top, S1 done, S2 start, S2 done,
- * S3 start, S3 done, then adjacency-load latency probes. */
+ * S3 start, S3 done, then kernel-specific S1 internals (candidate-list
+ * kernel: list length read, list + key loads, warp min). */
 dg_status dg_peel_trace_arm(uint32_t first_batch);
 dg_status dg_peel_trace_read(uint64_t out[8 * 32 * 12]);
 /* Diagnostic: block-0 cycles of the last coreness launch in level-advance min

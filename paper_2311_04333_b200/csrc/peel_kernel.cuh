@@ -161,40 +161,18 @@ __device__ __forceinline__ void stamp(unsigned long long* prof, unsigned long lo
 // S3 over one member's row for warps [rank] of the nwj serving it: the row
 // [oj, oj + dj) as 16-byte quads indexed relative to its first quad; only the
 // first and last quad can be partial.
-template <class K, bool SMEM, bool ONE, bool TR>
+template <class K, bool SMEM, bool ONE>
 __device__ __forceinline__ void remove_row(const uint4* adj4, K* keys, uint32_t keys_s,
                                            uint64_t oj, uint32_t dj, uint32_t vj, uint32_t rank,
-                                           uint32_t nwj, uint32_t lane, uint32_t* cnt,
-                                           unsigned long long* prof = nullptr,
-                                           unsigned long long tr_first = 0,
-                                           unsigned long long nbat = 0, uint32_t w = 0) {
+                                           uint32_t nwj, uint32_t lane, uint32_t* cnt) {
   const uint4* row = adj4 + (oj >> 2);
   const uint32_t head = uint32_t(oj & 3), end = head + dj;  // valid elements [head, end)
   const uint32_t nq = (end + 3) >> 2, stride = nwj * 32;
   for (uint32_t b = rank * 32 + lane; b < nq; b += stride * UQ) {
     uint4 x[UQ];
-    const bool tr = TR && tr_first && b - lane == rank * 32;  // warp-uniform: first pass
-    if (tr && lane == 0) stamp(prof, tr_first, nbat, w, 6, 0);
 #pragma unroll
     for (int k = 0; k < UQ; ++k)
       if (b + k * stride < nq) x[k] = __ldg(row + b + k * stride);
-    if (TR && tr) {  // probes: every lane's data must have arrived (warp-wide dependency)
-      const uint32_t am = __activemask();  // lanes with b < nq (lane 0 among them)
-      const uint32_t d0 = __reduce_or_sync(am, x[0].x);
-      if (lane == 0) stamp(prof, tr_first, nbat, w, 7, d0);
-      uint4 y = make_uint4(0, 0, 0, 0);  // the same quads again, L2 only
-      asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w)
-                   : "l"(row + b));
-      const uint32_t d1 = __reduce_or_sync(am, y.x);
-      if (lane == 0) stamp(prof, tr_first, nbat, w, 8, d1);
-      uint4 z = make_uint4(0, 0, 0, 0);  // full-warp quads 256 KB away
-      asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(z.x), "=r"(z.y), "=r"(z.z), "=r"(z.w)
-                   : "l"(row + b + 16 * 1024));
-      const uint32_t d2 = __reduce_or_sync(am, z.x);
-      if (lane == 0) stamp(prof, tr_first, nbat, w, 9, d2);
-    }
 #pragma unroll
     for (int k = 0; k < UQ; ++k) {
       const uint32_t t = b + k * stride;
@@ -426,11 +404,10 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
       PK_STAMP(3, 0);
       PK_STAMP(4, vj);
       if (bs == 1)
-        remove_row<K, SMEM, true, TR>(adj4, keys, keys_s, oj, dj, vj, rank, nwj, lane, nullptr,
-                                      a.prof, tr_first, nbat, w);
+        remove_row<K, SMEM, true>(adj4, keys, keys_s, oj, dj, vj, rank, nwj, lane, nullptr);
       else
-        remove_row<K, SMEM, false, TR>(adj4, keys, keys_s, oj, dj, vj, rank, nwj, lane,
-                                       &cnt[j], a.prof, tr_first, nbat, w);
+        remove_row<K, SMEM, false>(adj4, keys, keys_s, oj, dj, vj, rank, nwj, lane,
+                                       &cnt[j]);
       PK_STAMP(5, 0);
       __syncthreads();  // C
       pend_n = bs;
@@ -519,11 +496,11 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
         const uint32_t j = wm3 & 0xffu, rank = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
         PK_STAMP(4, wm3);
         if (bs == 1)
-          remove_row<K, SMEM, true, TR>(adj4, keys, keys_s, s.boff[0], s.bdeg[0], 0, rank, nwj,
-                                        lane, nullptr, a.prof, tr_first, nbat, w);
+          remove_row<K, SMEM, true>(adj4, keys, keys_s, s.boff[0], s.bdeg[0], 0, rank, nwj,
+                                        lane, nullptr);
         else  // the returned key tells same-batch neighbours apart
-          remove_row<K, SMEM, false, TR>(adj4, keys, keys_s, s.boff[j], s.bdeg[j], s.bv[j], rank,
-                                         nwj, lane, &s.cnt[j], a.prof, tr_first, nbat, w);
+          remove_row<K, SMEM, false>(adj4, keys, keys_s, s.boff[j], s.bdeg[j], s.bv[j], rank,
+                                         nwj, lane, &s.cnt[j]);
         PK_STAMP(5, 0);
         __syncthreads();  // C
         pend_n = bs;
