@@ -72,6 +72,20 @@ class TorchComm:
     def allreduce_min(self, x: int) -> int:
         return self._scalar(x, self.dist.ReduceOp.MIN)
 
+    def allreduce_max(self, x: int) -> int:
+        return self._scalar(x, self.dist.ReduceOp.MAX)
+
+    def allreduce_sum_tensor(self, t):
+        t = t.clone()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return t
+
+    def allgather_counts(self, counts: Sequence[int]) -> List[int]:
+        t = self.torch.tensor([int(counts[0])], dtype=self.torch.int64, device=self.device)
+        out = [self.torch.empty_like(t) for _ in range(self.P)]
+        self.dist.all_gather(out, t)
+        return [int(x.item()) for x in out]
+
     def alltoall_counts(self, counts: Sequence[Sequence[int]]) -> List[List[int]]:
         t = self.torch.tensor(list(counts[0]), dtype=self.torch.int64, device=self.device)
         out = self.torch.empty_like(t)
@@ -107,6 +121,15 @@ class LocalComm:
 
     def allreduce_min(self, x: int) -> int:
         return x
+
+    def allreduce_max(self, x: int) -> int:
+        return x
+
+    def allreduce_sum_tensor(self, t):
+        return t.clone()
+
+    def allgather_counts(self, counts: Sequence[int]) -> List[int]:
+        return [int(c) for c in counts]
 
     def alltoall_counts(self, counts):
         return [[counts[s][d] for s in range(self.P)] for d in range(self.P)]

@@ -1,0 +1,150 @@
+"""Distributed CSR build ("the CSR build shards the same way").
+
+Every rank holds a slice of the sample pairs (u, v) -- e.g. its share of a
+seeded generator's stream -- and ends with ITS rows of exactly the CSR that
+parse_edge_list / dg_graph_build would build from all pairs on one machine
+(io.cpp:51-92: loops dropped, duplicates merged, dense id = rank of the
+original id among present ones, rows ascending).  Protocol (collectives over
+`Comm`, the same objects as sharded.py, so NCCL on GPUs and gloo on CPU):
+
+  1  canonical pairs, loops dropped (local)
+  2  owner ranges of the ORIGINAL id space: all-reduced 4096-bucket histogram
+     of arc endpoints -> split points balancing arcs per rank; the dense
+     relabel is monotone, so original-id ranges are dense-id ranges
+  3  both arc directions routed to the owner of their source (all-to-all)
+  4  per rank: sort (src, dst), unique -> rows in ascending dst order; the
+     present vertices are the distinct sources
+  5  dense ids: exclusive scan of the per-rank vertex counts (all-gather)
+  6  neighbour ids: the distinct dsts are sent to their owners, answered with
+     dense ids (binary search in the owner's sorted vertices), returned
+     (all-to-all twice)
+
+Tensor work is torch on the device of the communicator (CUB sorts on GPUs).
+Original ids must be below 2^32 (the generators' ranges).  Result: the
+global vertex count n, the dense-id split points bounds[0..P] and per local
+shard (offs, adj, orig): offs rebased to 0 (n_r + 1 entries), adj = global
+dense ids (uint32), orig = original ids of the rank's vertices -- the input of
+CudaShard.from_rows (dg_shard_create_rows).
+"""
+from __future__ import annotations
+
+from typing import List, Sequence
+
+import numpy as np
+
+__all__ = ["build_shards", "coreness_from_pairs_distributed"]
+
+NB = 4096  # endpoint histogram buckets
+
+
+def _alltoallv(comm, sends, send_counts):
+    """all-to-all of one int64 tensor per local shard, split by send_counts."""
+    recv_counts = comm.alltoall_counts([list(map(int, c)) for c in send_counts])
+    return comm.alltoallv(sends, [list(map(int, c)) for c in send_counts], recv_counts)
+
+
+def build_shards(pairs: Sequence, comm):
+    """pairs: one (u, v) pair of int64 tensors per local shard (comm.shards()).
+    Returns (n, bounds, [(offs, adj, orig) numpy tuple per local shard])."""
+    import torch
+    P = comm.P
+    dev = pairs[0][0].device
+    # 1  canonical pairs, loops out
+    can = []
+    for u, v in pairs:
+        u = u.to(torch.int64)
+        v = v.to(torch.int64)
+        keep = u != v
+        a, b = torch.minimum(u, v)[keep], torch.maximum(u, v)[keep]
+        if a.numel() and int(b.max()) >= (1 << 32):
+            raise ValueError("distributed build: original ids must be below 2^32")
+        can.append((a, b))
+    # 2  owner ranges of the original id space
+    local_max = max([int(b.max()) if b.numel() else 0 for _, b in can] + [0])
+    idmax = comm.allreduce_max(local_max)
+    shift = 0
+    while (idmax >> shift) >= NB:
+        shift += 1
+    hist = torch.zeros(NB, dtype=torch.int64, device=dev)
+    for a, b in can:
+        hist += torch.bincount(a >> shift, minlength=NB)[:NB]
+        hist += torch.bincount(b >> shift, minlength=NB)[:NB]
+    hist = comm.allreduce_sum_tensor(hist)
+    cum = torch.cumsum(hist, 0).cpu().numpy()
+    total = int(cum[-1])
+    if total == 0:
+        raise ValueError("no edges after removing self-loops and duplicates")
+    # split[r] = first bucket of rank r (balanced arc counts)
+    split = np.searchsorted(cum, [(total * r) // P for r in range(P)], side="right")
+    split[0] = 0
+    split = np.maximum.accumulate(split)
+    bounds_id = [int(s) << shift for s in split] + [idmax + 1]  # original-id ranges
+
+    bnd = torch.tensor(bounds_id[1:-1], dtype=torch.int64, device=dev)
+
+    def owner(x):
+        return torch.bucketize(x, bnd, right=True)
+
+    # 3  route both arc directions to the owner of their source
+    sends, counts = [], []
+    for a, b in can:
+        src = torch.cat([a, b])
+        dst = torch.cat([b, a])
+        o = owner(src)
+        order = torch.argsort(o, stable=True)
+        # (src - 2^31) * 2^32 + dst: order-preserving in signed int64
+        packed = ((src[order] - (1 << 31)) << 32) | dst[order]
+        sends.append(packed)
+        counts.append(torch.bincount(o, minlength=P).cpu().tolist())
+    recvd = _alltoallv(comm, sends, counts)
+    # 4  rows: sort + unique; present vertices = distinct sources
+    rows = []
+    for k, r in enumerate(comm.shards()):
+        arcs = torch.unique(recvd[k])  # sorted, duplicates merged
+        src = (arcs >> 32) + (1 << 31)
+        dst = arcs & 0xFFFFFFFF
+        verts, deg = torch.unique_consecutive(src, return_counts=True)
+        rows.append((verts, deg, dst))
+    # 5  dense ids: exclusive scan of the vertex counts over ranks
+    counts_v = comm.allgather_counts([int(v.numel()) for v, _, _ in rows])
+    base = np.concatenate([[0], np.cumsum(counts_v)[:-1]]).astype(np.int64)
+    # 6  neighbour ids: ask the owners for the dense ids of the distinct dsts
+    qs, qcounts, inv = [], [], []
+    for verts, deg, dst in rows:
+        udst, iv = torch.unique(dst, return_inverse=True)
+        o = owner(udst)  # udst is sorted and owners ascend with ids: already grouped
+        qs.append(udst)
+        qcounts.append(torch.bincount(o, minlength=P).cpu().tolist())
+        inv.append(iv)
+    asked = _alltoallv(comm, qs, qcounts)
+    answers = []
+    for k, r in enumerate(comm.shards()):
+        verts = rows[k][0]
+        pos = torch.searchsorted(verts, asked[k])
+        answers.append(pos + int(base[r]))
+    # the answers go back along the reverse routes, in the askers' order
+    back_counts = comm.alltoall_counts([list(map(int, c)) for c in qcounts])
+    back = comm.alltoallv(answers, back_counts, [list(map(int, c)) for c in qcounts])
+    out = []
+    for k, r in enumerate(comm.shards()):
+        verts, deg, dst = rows[k]
+        dense = back[k][inv[k]]
+        offs = torch.zeros(verts.numel() + 1, dtype=torch.int64, device=dev)
+        offs[1:] = torch.cumsum(deg, 0)
+        out.append((offs.cpu().numpy().astype(np.uint64), dense.cpu().numpy().astype(np.uint32),
+                    verts.cpu().numpy().astype(np.uint64)))
+    n = int(sum(counts_v))
+    bounds = np.concatenate([base, [n]]).astype(np.uint64)
+    return n, bounds, out
+
+
+def coreness_from_pairs_distributed(u, v, approx=None):
+    """One rank's slice of the sample pairs (CUDA tensors) -> distributed CSR
+    build -> sharded coreness (NCCL).  Every rank gets all labels."""
+    import torch
+    from .sharded import CudaShard, TorchComm, _decomposition, sharded_coreness
+    comm = TorchComm(torch.device("cuda", torch.cuda.current_device()))
+    n, bounds, ((offs, adj, _orig),) = build_shards([(u, v)], comm)
+    shard = CudaShard.from_rows(n, bounds, comm.rank, offs, adj)
+    labs, kmax, rounds = sharded_coreness([shard], comm, n, approx)
+    return _decomposition(np.concatenate(comm.allgather(labs[0])), kmax, rounds, approx)

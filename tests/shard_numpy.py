@@ -23,6 +23,15 @@ class NumpyShard:
         self.front = np.zeros(0, np.int64)
         self.next = []
 
+    @classmethod
+    def from_rows(cls, n, bounds, rank, offs, adj):
+        """The rank's own rows only (offs rebased to 0): nothing outside
+        [lo, hi] of the global offsets is ever read."""
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        g = np.zeros(n + 1, np.int64)
+        g[lo:hi + 1] = np.asarray(offs, np.int64)
+        return cls(g, adj, bounds, rank)
+
     @property
     def n_local(self):
         return self.hi - self.lo

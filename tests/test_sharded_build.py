@@ -1,0 +1,164 @@
+"""Distributed CSR build (sharded_build.py): every rank starts
+from a slice of the sample pairs and ends with its rows of exactly the CSR the
+oracle builds from all pairs (io.cpp:51-92: loops dropped, duplicates merged,
+dense ids = rank of the original id).  CPU: in-process shards and a
+world_size-2 gloo run, then coreness over the built shards vs the oracle;
+GPU: the same on CUDA tensors feeding the CUDA shard kernels."""
+import os
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+from shard_numpy import NumpyShard
+from test_sharded import _free_port
+
+from paper_2311_04333_b200.sharded import LocalComm, TorchComm, sharded_coreness
+from paper_2311_04333_b200.sharded_build import build_shards
+
+
+def _cases(orc):
+    rng = np.random.default_rng(11)
+    out = {
+        "rmat12": orc.gen_rmat(12, 64 * 1024, 3),
+        "chung_lu": orc.gen_chung_lu(3000, 20000, 5),
+        "planted": orc.gen_er_planted(2000, 6000, 30, 5),
+    }
+    # duplicates (both orientations), self-loops and ids spread up to 2^32-1
+    ids = np.unique(np.concatenate([rng.integers(0, 1 << 32, 400, dtype=np.uint64),
+                                    np.array([0, (1 << 32) - 1], np.uint64)]))
+    a = ids[rng.integers(0, len(ids), 3000)]
+    b = ids[rng.integers(0, len(ids), 3000)]
+    u = np.concatenate([a, b, a[:50], a[:40]])
+    v = np.concatenate([b, a, b[:50], a[:40]])
+    out["sparse_ids_dups_loops"] = (u, v)
+    return out
+
+
+def _split(u, v, P, skew=False):
+    """Sample slices per rank; skew=True puts everything on the last rank."""
+    if skew:
+        cuts = [0] * P + [len(u)]
+    else:
+        cuts = np.linspace(0, len(u), P + 1).astype(int)
+    return [(torch.from_numpy(np.asarray(u[cuts[i]:cuts[i + 1]], np.int64)),
+             torch.from_numpy(np.asarray(v[cuts[i]:cuts[i + 1]], np.int64))) for i in range(P)]
+
+
+def _assemble(sh):
+    base, offs = 0, [np.zeros(1, np.uint64)]
+    for o, _, _ in sh:
+        offs.append(o[1:] + np.uint64(base))
+        base += int(o[-1])
+    return (np.concatenate(offs), np.concatenate([s[1] for s in sh]),
+            np.concatenate([s[2] for s in sh]))
+
+
+def _check_csr(g, n, bounds, sh):
+    offs, adj, orig = _assemble(sh)
+    assert n == g.n and int(bounds[-1]) == n and bounds[0] == 0
+    np.testing.assert_array_equal(offs, g.offs)
+    np.testing.assert_array_equal(adj, g.adj)
+    np.testing.assert_array_equal(orig, g.orig)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+def test_build_local_matches_oracle(orc, P):
+    for name, (u, v) in _cases(orc).items():
+        g = orc.build(u, v)
+        for skew in (False, True):
+            n, bounds, sh = build_shards(_split(u, v, P, skew), LocalComm(P, "cpu"))
+            _check_csr(g, n, bounds, sh)
+            # coreness over the rank-owned rows = the oracle's
+            shards = [NumpyShard.from_rows(n, bounds, r, sh[r][0], sh[r][1]) for r in range(P)]
+            labs, kmax, rounds = sharded_coreness(shards, LocalComm(P, "cpu"), n)
+            lab, k, rr = orc.coreness(g)
+            np.testing.assert_array_equal(np.concatenate(labs), lab)
+            assert (kmax, rounds) == (k, rr)
+
+
+def test_build_balances_arcs(orc):
+    u, v = orc.gen_rmat(14, 16 << 14, 8)
+    g = orc.build(u, v)
+    P = 4
+    n, bounds, sh = build_shards(_split(u, v, P), LocalComm(P, "cpu"))
+    arcs = np.array([int(o[-1]) for o, _, _ in sh])
+    assert arcs.sum() == int(g.offs[-1])
+    # bucket-granular split: within 25% of the ideal share on RMAT-14
+    assert arcs.max() <= 1.25 * arcs.sum() / P
+
+
+def test_build_rejects_bad_input():
+    z = torch.zeros(0, dtype=torch.int64)
+    with pytest.raises(ValueError, match="no edges"):
+        build_shards([(torch.tensor([3, 4]), torch.tensor([3, 4])), (z, z)], LocalComm(2, "cpu"))
+    with pytest.raises(ValueError, match="2\\^32"):
+        build_shards([(torch.tensor([0]), torch.tensor([1 << 32]))], LocalComm(1, "cpu"))
+
+
+def _gloo_worker(rank, world, port, outdir):
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "oracle"))
+    import torch.distributed as dist
+    from oracle import Oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        res = {}
+        for name, (u, v) in _cases(orc).items():
+            comm = TorchComm("cpu")
+            n, bounds, sh = build_shards([_split(u, v, world)[rank]], comm)
+            shard = NumpyShard.from_rows(n, bounds, rank, sh[0][0], sh[0][1])
+            labs, kmax, rounds = sharded_coreness([shard], comm, n)
+            parts = comm.allgather((sh[0], labs[0]))
+            res[name] = (n, bounds, [p[0] for p in parts], np.concatenate([p[1] for p in parts]),
+                         kmax, rounds)
+        if rank == 0:
+            np.save(os.path.join(outdir, "res.npy"), res, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_build_gloo_world2(orc):
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gloo_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = np.load(os.path.join(d, "res.npy"), allow_pickle=True).item()
+    for name, (u, v) in _cases(orc).items():
+        g = orc.build(u, v)
+        n, bounds, sh, labels, kmax, rounds = res[name]
+        _check_csr(g, n, bounds, sh)
+        lab, k, rr = orc.coreness(g)
+        np.testing.assert_array_equal(labels, lab)
+        assert (kmax, rounds) == (k, rr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 3, 8])
+def test_build_cuda_shards(orc, dg, P):
+    """CUDA tensors through the build, rows into the CUDA shard kernels."""
+    from paper_2311_04333_b200.sharded import CudaShard
+    for name, (u, v) in _cases(orc).items():
+        g = orc.build(u, v)
+        pairs = [(a.cuda(), b.cuda()) for a, b in _split(u, v, P)]
+        n, bounds, sh = build_shards(pairs, LocalComm(P))
+        _check_csr(g, n, bounds, sh)
+        shards = [CudaShard.from_rows(n, bounds, r, sh[r][0], sh[r][1]) for r in range(P)]
+        labs, kmax, rounds = sharded_coreness(shards, LocalComm(P), n)
+        lab, k, rr = orc.coreness(g)
+        np.testing.assert_array_equal(np.concatenate(labs), lab)
+        assert (kmax, rounds) == (k, rr)
+
+
+@pytest.mark.gpu
+def test_build_cuda_rmat18(orc, dg):
+    u, v = orc.gen_rmat(18, 16 << 18, 21)
+    g = orc.build(u, v)
+    P = 4
+    pairs = [(a.cuda(), b.cuda()) for a, b in _split(u, v, P)]
+    n, bounds, sh = build_shards(pairs, LocalComm(P))
+    _check_csr(g, n, bounds, sh)
