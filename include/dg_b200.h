@@ -192,6 +192,21 @@ dg_status dg_run(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res
                  dg_iter_record* trace, uint64_t trace_cap, uint64_t* witness,
                  uint64_t witness_cap, uint64_t* final_ids, uint64_t final_cap);
 
+/* run() continued after a first prune done elsewhere (framework.cpp:92-180):
+ * `core` = get_core(input, labels, threshold) where threshold follows from
+ * kmax and cfg->pruning as in framework.cpp:62-79, core_labels (host, core->n)
+ * are the coreness labels of the core's vertices, peel_rounds those of the
+ * coreness pass.  Produced by the sharded pipeline (sharded coreness +
+ * per-shard compaction, one gather); identical result to dg_run on the input
+ * graph (the witness recount on the core equals the one on the input: the
+ * core is an induced subgraph containing the witness).  pruning 3 (hybrid)
+ * runs its exact pass on the core here.  DG_E_INVARIANT if a label is below
+ * the threshold, DG_E_PARAM for pruning 0. */
+dg_status dg_run_pruned(const dg_graph* core, const uint32_t* core_labels, uint32_t kmax,
+                        uint32_t peel_rounds, const dg_run_config* cfg, dg_run_result* res,
+                        dg_iter_record* trace, uint64_t trace_cap, uint64_t* witness,
+                        uint64_t witness_cap, uint64_t* final_ids, uint64_t final_cap);
+
 /* ------------------------------------------------------------ sharded coreness */
 
 /* One GPU's shard of a 1D vertex-range-partitioned exact coreness

@@ -30,7 +30,7 @@ __all__ = [
     "RefineOutcome", "RunConfig", "RunResult", "RunTrace", "IterRecord", "InitRecord",
     "parse_edge_list", "parse_edge_list_file", "induced_subgraph", "exact_coreness", "approx_coreness", "get_core",
     "load_peel_order", "load_sort_order", "density_and_load_update", "charikar_peel",
-    "slack_violations", "default_iterations", "run", "gen_rmat", "gen_chung_lu",
+    "slack_violations", "default_iterations", "run", "run_pruned", "gen_rmat", "gen_chung_lu",
     "DensegraphError", "ParseError", "EmptyGraphError", "IoError", "ParamError",
     "InvariantError", "OracleSizeError", "CacheHashError", "kNoVertex", "format_fixed6",
     "ceil_div", "ceil_scaled", "mix64",
@@ -532,7 +532,7 @@ def synchronize() -> None:
     _chk(LIB.dg_synchronize())
 
 
-def run(g: Graph, cfg: Optional[RunConfig] = None) -> RunResult:
+def _run(g: Graph, cfg: Optional[RunConfig], pruned=None) -> RunResult:
     cfg = cfg or RunConfig()
     res = DgRunResult()
     cap = 1 << 16
@@ -540,8 +540,16 @@ def run(g: Graph, cfg: Optional[RunConfig] = None) -> RunResult:
     wit = np.zeros(max(g.n, 1), np.uint64)
     fin = np.zeros(max(g.n, 1), np.uint64)
     c = cfg.to_c()
-    _chk(LIB.dg_run(g._h, C.byref(c), C.byref(res), trace, cap, _p(wit, u64p), g.n,
-                    _p(fin, u64p), g.n))
+    if pruned is None:
+        _chk(LIB.dg_run(g._h, C.byref(c), C.byref(res), trace, cap, _p(wit, u64p), g.n,
+                        _p(fin, u64p), g.n))
+    else:
+        labels, kmax, rounds = pruned
+        lab = np.ascontiguousarray(labels, dtype=np.uint32)
+        if len(lab) != g.n:
+            raise InvariantError("core labels do not match graph size")
+        _chk(LIB.dg_run_pruned(g._h, _p(lab, u32p), kmax, rounds, C.byref(c), C.byref(res),
+                               trace, cap, _p(wit, u64p), g.n, _p(fin, u64p), g.n))
     iters = [IterRecord(t.iter, Density(t.rho_edges, t.rho_verts), t.n, t.m, t.width, t.ms,
                         t.order_ms, t.update_ms, t.batches)
              for t in trace[: min(res.iterations, cap)]]
@@ -552,6 +560,20 @@ def run(g: Graph, cfg: Optional[RunConfig] = None) -> RunResult:
     return RunResult(Density(res.best_edges, res.best_verts), wit[: res.witness_size].copy(),
                      res.witness_edges, res.iterations, res.max_width, res.total_ms, tr,
                      res.reprunes, res.reprune_ms, res.device_ms)
+
+
+def run(g: Graph, cfg: Optional[RunConfig] = None) -> RunResult:
+    """run(g, cfg) (framework.cpp:46-180)."""
+    return _run(g, cfg)
+
+
+def run_pruned(core: Graph, labels, kmax: int, peel_rounds: int,
+               cfg: Optional[RunConfig] = None) -> RunResult:
+    """run() continued from a first prune computed elsewhere (framework.cpp:92
+    onwards): `core` = get_core(input, dec, threshold(kmax)) with its labels --
+    what the sharded coreness and per-shard compaction produce
+    (sharded_build.run_distributed).  Same result as run() on the input."""
+    return _run(core, cfg, (labels, kmax, peel_rounds))
 
 
 # ------------------------------------------------------------------ synthetic inputs

@@ -76,6 +76,9 @@ PROTOTYPES = {
     "dg_run": (C.c_int, [GP, C.POINTER(DgRunConfig), C.POINTER(DgRunResult),
                          C.POINTER(DgIterRecord), C.c_uint64, u64p, C.c_uint64, u64p,
                          C.c_uint64]),
+    "dg_run_pruned": (C.c_int, [GP, u32p, C.c_uint32, C.c_uint32, C.POINTER(DgRunConfig),
+                                C.POINTER(DgRunResult), C.POINTER(DgIterRecord), C.c_uint64,
+                                u64p, C.c_uint64, u64p, C.c_uint64]),
     "dg_shard_create": (C.c_int, [GP, u64p, C.c_uint32, C.c_uint32, GPP]),
     "dg_shard_create_rows": (C.c_int, [C.c_uint64, u64p, C.c_uint32, C.c_uint32, u64p, u32p,
                                        C.c_int, GPP]),

@@ -163,9 +163,17 @@ struct Events {
   }
 };
 
+// The first prune computed elsewhere (the sharded coreness + per-shard
+// compaction of sharded.py): `core` = get_core(input, labels, threshold) and
+// its labels; run_impl then continues exactly as framework.cpp:92 onwards.
+struct Pruned {
+  const uint32_t* labels;  // host, core->n entries
+  uint32_t kmax, rounds;
+};
+
 void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
               dg_iter_record* trace, uint64_t trace_cap, uint64_t* witness, uint64_t witness_cap,
-              uint64_t* final_ids, uint64_t final_cap) {
+              uint64_t* final_ids, uint64_t final_cap, const Pruned* pre = nullptr) {
   if (!g || !cfg || !res) throw DgError(DG_E_PARAM, "null argument");
   if (g->n == 0) throw DgError(DG_E_EMPTY, "run on empty graph");
   if (cfg->algorithm < 0 || cfg->algorithm > 1 || cfg->pruning < 0 || cfg->pruning > 3)
@@ -180,7 +188,47 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
   bool approx_labels = false;
   uint64_t thresh = 0, le = 0, lv = 1;  // lower = {0,1}
 
-  if (cfg->pruning != 0) {
+  auto hybrid = [&](const dg_graph& base) {  // framework.cpp:80-91
+    DevBuf<uint32_t> fine(base.n), map2(base.n);
+    CoreOut cf = coreness(base, false, 1, 1, fine.get());
+    res->coreness_kernel_ms += cf.kernel_ms;
+    le = cf.kmax;
+    lv = 2;
+    thresh = ceil_scaled(le, lv, 1, 1);
+    GraphPtr next = induced(base, nullptr, fine.get(), uint32_t(thresh), map2.get());
+    labels.alloc(next->n);
+    gather_by_map_u32(fine.get(), map2.get(), base.n, labels.get());
+    owned = std::move(next);
+    approx_labels = false;
+    res->kmax_exact = 1;
+    res->kmax = cf.kmax;
+    res->threshold = uint32_t(thresh);
+  };
+  if (pre) {
+    if (cfg->pruning == 0) throw DgError(DG_E_PARAM, "a pre-pruned core needs a pruning mode");
+    if (!pre->labels) throw DgError(DG_E_PARAM, "null core labels");
+    const double c0 = now_ms();
+    const bool approx = cfg->pruning != 1;
+    res->peel_rounds = pre->rounds;
+    le = pre->kmax;
+    lv = 2;
+    thresh = approx ? ceil_scaled(le, lv, cfg->c_den, cfg->c_num) : ceil_scaled(le, lv, 1, 1);
+    for (uint64_t v = 0; v < g->n; ++v)
+      if (pre->labels[v] < thresh)
+        throw DgError(DG_E_INVARIANT, "core vertex below the pruning threshold");
+    labels.alloc(g->n);
+    h2d(labels.get(), pre->labels, g->n);
+    approx_labels = approx;
+    res->kmax_known = 1;
+    res->kmax_exact = !approx;
+    res->kmax = pre->kmax;
+    res->threshold = uint32_t(thresh);
+    if (cfg->pruning == 3) hybrid(*g);
+    cur = owned ? owned.get() : g;
+    stream_sync();
+    res->coreness_ms = now_ms() - c0;
+    if (cur->n == 0) throw DgError(DG_E_INVARIANT, "pruning removed every vertex");
+  } else if (cfg->pruning != 0) {
     const double c0 = now_ms();
     const bool approx = cfg->pruning != 1;
     DevBuf<uint32_t> lab(g->n), map(g->n);
@@ -199,21 +247,9 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
     res->kmax_exact = !approx;
     res->kmax = co.kmax;
     res->threshold = uint32_t(thresh);
-    if (cfg->pruning == 3) {  // hybrid, framework.cpp:80-91
-      DevBuf<uint32_t> fine(owned->n), map2(owned->n);
-      CoreOut cf = coreness(*owned, false, 1, 1, fine.get());
-      res->coreness_kernel_ms += cf.kernel_ms;
-      le = cf.kmax;
-      lv = 2;
-      thresh = ceil_scaled(le, lv, 1, 1);
-      GraphPtr next = induced(*owned, nullptr, fine.get(), uint32_t(thresh), map2.get());
-      labels.alloc(next->n);
-      gather_by_map_u32(fine.get(), map2.get(), owned->n, labels.get());
-      owned = std::move(next);
-      approx_labels = false;
-      res->kmax_exact = 1;
-      res->kmax = cf.kmax;
-      res->threshold = uint32_t(thresh);
+    if (cfg->pruning == 3) {
+      GraphPtr first = std::move(owned);
+      hybrid(*first);
     }
     cur = owned.get();
     stream_sync();
@@ -676,6 +712,16 @@ dg_status dg_run(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res
                  uint64_t witness_cap, uint64_t* final_ids, uint64_t final_cap) {
   DG_API_BEGIN
   run_impl(g, cfg, res, trace, trace_cap, witness, witness_cap, final_ids, final_cap);
+  DG_API_END
+}
+
+dg_status dg_run_pruned(const dg_graph* core, const uint32_t* core_labels, uint32_t kmax,
+                        uint32_t peel_rounds, const dg_run_config* cfg, dg_run_result* res,
+                        dg_iter_record* trace, uint64_t trace_cap, uint64_t* witness,
+                        uint64_t witness_cap, uint64_t* final_ids, uint64_t final_cap) {
+  DG_API_BEGIN
+  Pruned pre{core_labels, kmax, peel_rounds};
+  run_impl(core, cfg, res, trace, trace_cap, witness, witness_cap, final_ids, final_cap, &pre);
   DG_API_END
 }
 

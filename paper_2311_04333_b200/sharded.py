@@ -105,6 +105,17 @@ class TorchComm:
         self.dist.all_gather_object(objs, arr)
         return objs
 
+    def allgatherv(self, ts):
+        """Variable-length all-gather of one tensor per local shard -> P tensors."""
+        t = ts[0]
+        sizes = self.allgather_counts([t.numel()])
+        cap = max(sizes + [1])
+        pad = self.torch.zeros(cap, dtype=t.dtype, device=self.device)
+        pad[: t.numel()] = t
+        out = [self.torch.empty_like(pad) for _ in range(self.P)]
+        self.dist.all_gather(out, pad)
+        return [o[:c] for o, c in zip(out, sizes)]
+
 
 class LocalComm:
     """All P shards in this process (single-GPU validation of the shard kernels)."""
@@ -146,6 +157,9 @@ class LocalComm:
 
     def allgather(self, arrs):
         return arrs
+
+    def allgatherv(self, ts):
+        return list(ts)
 
 
 # ------------------------------------------------------------------ CUDA shard engine

@@ -32,7 +32,8 @@ from typing import List, Sequence
 
 import numpy as np
 
-__all__ = ["build_shards", "coreness_from_pairs_distributed"]
+__all__ = ["build_shards", "coreness_from_pairs_distributed", "shard_get_core", "gather_rows",
+           "prune_distributed", "run_distributed"]
 
 NB = 4096  # endpoint histogram buckets
 
@@ -148,3 +149,97 @@ def coreness_from_pairs_distributed(u, v, approx=None):
     shard = CudaShard.from_rows(n, bounds, comm.rank, offs, adj)
     labs, kmax, rounds = sharded_coreness([shard], comm, n, approx)
     return _decomposition(np.concatenate(comm.allgather(labs[0])), kmax, rounds, approx)
+
+
+# ------------------------------------------------------------------ per-shard get_core
+def shard_get_core(comm, bounds, rows, labels, k: int):
+    """get_core (core.cpp:133-140 -> induced_subgraph, graph.hpp:50-80) on the
+    shards: each rank keeps its vertices with label >= k; new dense ids =
+    exclusive scan of the kept counts over ranks (old order preserved); the
+    old->new map is all-gathered (4 B per vertex) so every rank renames its
+    kept arcs locally.  rows / labels: per local shard (offs, adj, orig) and
+    labels (numpy or tensors).  Returns (n', bounds', rows', labels')."""
+    import torch
+    dev = comm.device
+    keeps, maps_local = [], []
+    kept = [int((torch.as_tensor(np.asarray(l, np.int64)) >= k).sum()) for l in labels]
+    counts = comm.allgather_counts(kept)
+    base = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+    for (r, lab) in zip(comm.shards(), labels):
+        keep = torch.as_tensor(np.asarray(lab, np.int64), device=dev) >= k
+        new = torch.cumsum(keep.to(torch.int64), 0) - 1 + int(base[r])
+        keeps.append(keep)
+        maps_local.append(torch.where(keep, new, torch.full_like(new, -1)))
+    full = torch.cat(comm.allgatherv(maps_local))
+    out_rows, out_labels = [], []
+    for (offs, adj, orig), lab, keep in zip(rows, labels, keeps):
+        offs = torch.as_tensor(np.asarray(offs, np.int64), device=dev)
+        adj = torch.as_tensor(np.asarray(adj, np.int64), device=dev)
+        nl = offs.numel() - 1
+        row = torch.repeat_interleave(torch.arange(nl, device=dev), offs[1:] - offs[:-1])
+        nadj = full[adj] if adj.numel() else adj
+        ka = keep[row] & (nadj >= 0)
+        deg = torch.bincount(row[ka], minlength=nl)[keep]
+        noffs = torch.zeros(deg.numel() + 1, dtype=torch.int64, device=dev)
+        noffs[1:] = torch.cumsum(deg, 0)
+        out_rows.append((noffs.cpu().numpy().astype(np.uint64),
+                         nadj[ka].cpu().numpy().astype(np.uint32),
+                         np.asarray(orig, np.uint64)[keep.cpu().numpy()]))
+        out_labels.append(np.asarray(lab, np.uint32)[keep.cpu().numpy()])
+    n2 = int(sum(counts))
+    return n2, np.concatenate([base, [n2]]).astype(np.uint64), out_rows, out_labels
+
+
+def gather_rows(comm, rows, labels):
+    """All ranks get the whole (core) CSR: offs, adj, orig, labels (numpy)."""
+    import torch
+    dev = comm.device
+
+    def gat(arrs):
+        ts = [torch.as_tensor(np.asarray(a, np.int64), device=dev) for a in arrs]
+        return torch.cat(comm.allgatherv(ts)).cpu().numpy()
+
+    deg = gat([np.diff(np.asarray(o, np.int64)) for o, _, _ in rows])
+    offs = np.zeros(len(deg) + 1, np.uint64)
+    offs[1:] = np.cumsum(deg)
+    return (offs, gat([a for _, a, _ in rows]).astype(np.uint32),
+            gat([o for _, _, o in rows]).astype(np.uint64), gat(labels).astype(np.uint32))
+
+
+def prune_distributed(pairs, comm, make_shard, cfg):
+    """framework.cpp:58-79 on the shards: distributed build, sharded coreness
+    (exact, or approximate for approx/hybrid), first threshold, per-shard
+    get_core, one gather.  Returns (core offs, adj, orig, core labels, kmax,
+    peel_rounds) on every rank -- the input of run_pruned.
+    make_shard(n, bounds, rank, offs, adj) -> a shard engine."""
+    from . import Density, ceil_scaled
+    from .sharded import sharded_coreness
+    if cfg.pruning == "none":
+        raise ValueError("the sharded pipeline prunes; use run() for pruning='none'")
+    approx = None if cfg.pruning == "exact" else (cfg.c_num, cfg.c_den)
+    n, bounds, rows = build_shards(pairs, comm)
+    shards = [make_shard(n, bounds, r, o, a) for r, (o, a, _) in zip(comm.shards(), rows)]
+    labs, kmax, rounds = sharded_coreness(shards, comm, n, approx)
+    del shards
+    lower = Density(kmax, 2)
+    thresh = ceil_scaled(lower, 1, 1) if approx is None else ceil_scaled(lower, cfg.c_den,
+                                                                         cfg.c_num)
+    _, _, crow, clab = shard_get_core(comm, bounds, rows, labs, thresh)
+    offs, adj, orig, lab = gather_rows(comm, crow, clab)
+    return offs, adj, orig, lab, kmax, rounds
+
+
+def run_distributed(u, v, cfg=None):
+    """run() over torch.distributed ranks (NCCL): this rank's slice of the
+    sample pairs (CUDA int64 tensors) -> distributed build -> sharded
+    coreness -> per-shard compaction -> the core gathered to every rank ->
+    Greedy++ replica (dg_run_pruned).  Same RunResult as run() on the graph
+    of all pairs."""
+    import torch
+    from . import Graph, RunConfig, run_pruned
+    from .sharded import CudaShard, TorchComm
+    cfg = cfg or RunConfig()
+    comm = TorchComm(torch.device("cuda", torch.cuda.current_device()))
+    offs, adj, orig, lab, kmax, rounds = prune_distributed([(u, v)], comm, CudaShard.from_rows,
+                                                           cfg)
+    return run_pruned(Graph.from_csr(offs, adj, orig), lab, kmax, rounds, cfg)

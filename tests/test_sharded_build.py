@@ -162,3 +162,121 @@ def test_build_cuda_rmat18(orc, dg):
     pairs = [(a.cuda(), b.cuda()) for a, b in _split(u, v, P)]
     n, bounds, sh = build_shards(pairs, LocalComm(P))
     _check_csr(g, n, bounds, sh)
+
+
+# ------------------------------------------------------------------ sharded prune pipeline
+PRUNINGS = ["exact", "approx", "hybrid"]
+
+
+def _expected_core(orc, g, pruning, c_num=3, c_den=2):
+    """framework.cpp:58-79 first prune on the whole graph (oracle)."""
+    approx = pruning != "exact"
+    lab, kmax, rounds = orc.coreness(g, approx, c_num, c_den) if approx else orc.coreness(g)
+    num, den = (1, 1) if not approx else (c_den, c_num)
+    p, q = kmax * num, 2 * den
+    thresh = p // q + (p % q != 0)
+    keep = lab >= thresh
+    core, _ = orc.get_core(g, lab, thresh)
+    return core, lab[keep], kmax, rounds
+
+
+def _check_core(orc, g, pruning, got):
+    offs, adj, orig, lab, kmax, rounds = got
+    core, elab, ek, er = _expected_core(orc, g, pruning)
+    np.testing.assert_array_equal(offs, core.offs)
+    np.testing.assert_array_equal(adj, core.adj)
+    np.testing.assert_array_equal(orig, core.orig)
+    np.testing.assert_array_equal(lab, elab)
+    assert (kmax, rounds) == (ek, er)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_prune_local_matches_oracle(orc, P):
+    from oracle import RunConfig
+    from paper_2311_04333_b200.sharded_build import prune_distributed
+    for name, (u, v) in _cases(orc).items():
+        g = orc.build(u, v)
+        for pruning in PRUNINGS:
+            got = prune_distributed(_split(u, v, P), LocalComm(P, "cpu"), NumpyShard.from_rows,
+                                    RunConfig(pruning=pruning))
+            _check_core(orc, g, pruning, got)
+
+
+def test_prune_rejects_none(orc):
+    from oracle import RunConfig
+    from paper_2311_04333_b200.sharded_build import prune_distributed
+    u, v = _cases(orc)["planted"]
+    with pytest.raises(ValueError):
+        prune_distributed(_split(u, v, 2), LocalComm(2, "cpu"), NumpyShard.from_rows,
+                          RunConfig(pruning="none"))
+
+
+def _gloo_prune_worker(rank, world, port, outdir):
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "oracle"))
+    import torch.distributed as dist
+    from oracle import Oracle, RunConfig
+    from paper_2311_04333_b200.sharded_build import prune_distributed
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        res = {}
+        for name, (u, v) in _cases(orc).items():
+            for pruning in PRUNINGS:
+                res[f"{name}/{pruning}"] = prune_distributed(
+                    [_split(u, v, world)[rank]], TorchComm("cpu"), NumpyShard.from_rows,
+                    RunConfig(pruning=pruning))
+        np.save(os.path.join(outdir, f"res{rank}.npy"), res, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_prune_gloo_world2(orc):
+    """Every rank ends with the same gathered core (the Greedy++ replicas' input)."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gloo_prune_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [np.load(os.path.join(d, f"res{r}.npy"), allow_pickle=True).item() for r in (0, 1)]
+    for name, (u, v) in _cases(orc).items():
+        g = orc.build(u, v)
+        for pruning in PRUNINGS:
+            for r in (0, 1):
+                _check_core(orc, g, pruning, res[r][f"{name}/{pruning}"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 4])
+def test_run_pruned_matches_run(orc, dg, P):
+    """Sharded prune on CUDA shards + dg_run_pruned = run() on the whole graph
+    = the oracle's run (best, witness, trace, final vertices, slack)."""
+    from oracle import RunConfig as ORC
+    from paper_2311_04333_b200.sharded import CudaShard
+    from paper_2311_04333_b200.sharded_build import prune_distributed
+    for name, (u, v) in _cases(orc).items():
+        hg = orc.build(u, v)
+        g = dg.Graph.from_csr(hg.offs, hg.adj, hg.orig)
+        for pruning in PRUNINGS:
+            for algorithm in ("peel", "sort"):
+                cfg = dg.RunConfig(algorithm=algorithm, pruning=pruning, iterations=6)
+                pairs = [(a.cuda(), b.cuda()) for a, b in _split(u, v, P)]
+                offs, adj, orig, lab, kmax, rounds = prune_distributed(
+                    pairs, LocalComm(P), CudaShard.from_rows, cfg)
+                got = dg.run_pruned(dg.Graph.from_csr(offs, adj, orig), lab, kmax, rounds, cfg)
+                want = dg.run(g, cfg)
+                ref = orc.run(hg, ORC(algorithm=algorithm, pruning=pruning, iterations=6))
+                assert got.best == want.best
+                assert (got.best.edges, got.best.verts) == tuple(ref.best)
+                np.testing.assert_array_equal(got.witness, want.witness)
+                assert got.witness_edges == want.witness_edges
+                assert [(t.rho, t.n, t.m, t.width) for t in got.trace.iters] == \
+                    [(t.rho, t.n, t.m, t.width) for t in want.trace.iters]
+                np.testing.assert_array_equal(got.trace.final_vertices,
+                                              want.trace.final_vertices)
+                i, j = got.trace.init, want.trace.init
+                assert (i.kmax, i.threshold, i.kmax_exact, i.pruned_n, i.pruned_m,
+                        i.peel_rounds) == (j.kmax, j.threshold, j.kmax_exact, j.pruned_n,
+                                           j.pruned_m, j.peel_rounds)
+                assert got.trace.slack_violations == want.trace.slack_violations
+                assert got.reprunes == want.reprunes
