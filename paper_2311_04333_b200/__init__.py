@@ -232,6 +232,21 @@ class Graph:
                                    C.byref(h)))
         return cls(h)
 
+    @classmethod
+    def from_device_csr(cls, offs, adj, orig) -> "Graph":
+        """CSR already on the GPU (torch CUDA tensors: int64 offsets, int32/uint32
+        ids, int64 original ids); copied into the library's graph."""
+        import torch
+        offs = offs.to(torch.int64).contiguous()
+        adj = adj.to(torch.int32).contiguous()
+        orig = orig.to(torch.int64).contiguous()
+        torch.cuda.synchronize()
+        h = C.c_void_p()
+        _chk(LIB.dg_graph_from_csr(orig.numel(), C.cast(C.c_void_p(offs.data_ptr()), u64p),
+                                   C.cast(C.c_void_p(adj.data_ptr()), u32p),
+                                   C.cast(C.c_void_p(orig.data_ptr()), u64p), 1, C.byref(h)))
+        return cls(h)
+
     # -- reference field access (tests read g.offs / g.adj / g.orig)
     def download(self):
         if self._host is None:

@@ -183,11 +183,23 @@ class CudaShard:
                                      C.byref(h)))
         else:
             n, offs, adj = rows
-            offs = np.ascontiguousarray(offs, dtype=np.uint64)
-            adj = np.ascontiguousarray(adj, dtype=np.uint32)
-            _chk(LIB.dg_shard_create_rows(n, self.bounds.ctypes.data_as(u64p), self.P, rank,
-                                          offs.ctypes.data_as(u64p), adj.ctypes.data_as(u32p), 0,
-                                          C.byref(h)))
+            if isinstance(offs, torch.Tensor) and offs.is_cuda:
+                # device rows (sharded_build): int64 offsets, int32 holding uint32 ids
+                offs = offs.to(torch.int64).contiguous()
+                adj = adj.to(torch.int32).contiguous()
+                torch.cuda.synchronize()  # produced on torch's stream, copied on the library's
+                _chk(LIB.dg_shard_create_rows(n, self.bounds.ctypes.data_as(u64p), self.P, rank,
+                                              C.cast(C.c_void_p(offs.data_ptr()), u64p),
+                                              C.cast(C.c_void_p(adj.data_ptr()), u32p), 1,
+                                              C.byref(h)))
+                _chk(LIB.dg_synchronize())  # copies done before torch may reuse the memory
+            else:
+                offs = np.ascontiguousarray(np.asarray(offs), dtype=np.uint64)
+                adj = np.ascontiguousarray(np.asarray(adj).astype(np.int64) & 0xFFFFFFFF,
+                                           dtype=np.uint32)
+                _chk(LIB.dg_shard_create_rows(n, self.bounds.ctypes.data_as(u64p), self.P, rank,
+                                              offs.ctypes.data_as(u64p), adj.ctypes.data_as(u32p),
+                                              0, C.byref(h)))
         self._h = h
 
     @classmethod

@@ -21,10 +21,11 @@ original id among present ones, rows ascending).  Protocol (collectives over
 
 Tensor work is torch on the device of the communicator (CUB sorts on GPUs).
 Original ids must be below 2^32 (the generators' ranges).  Result: the
-global vertex count n, the dense-id split points bounds[0..P] and per local
-shard (offs, adj, orig): offs rebased to 0 (n_r + 1 entries), adj = global
-dense ids (uint32), orig = original ids of the rank's vertices -- the input of
-CudaShard.from_rows (dg_shard_create_rows).
+global vertex count n, the dense-id split points bounds[0..P] (numpy) and per
+local shard (offs, adj, orig) as tensors on the communicator's device: offs
+int64 rebased to 0 (n_r + 1 entries), adj = global dense ids (int32 holding
+uint32 bits), orig int64 = original ids of the rank's vertices -- the input of
+CudaShard.from_rows (dg_shard_create_rows, device pointers).
 """
 from __future__ import annotations
 
@@ -92,9 +93,10 @@ def build_shards(pairs: Sequence, comm):
         src = torch.cat([a, b])
         dst = torch.cat([b, a])
         o = owner(src)
-        order = torch.argsort(o, stable=True)
         # (src - 2^31) * 2^32 + dst: order-preserving in signed int64
-        packed = ((src[order] - (1 << 31)) << 32) | dst[order]
+        packed = ((src - (1 << 31)) << 32) | dst
+        if P > 1:  # grouping only (the receiver sorts): a narrow key keeps the radix sort short
+            packed = packed[torch.argsort(o.to(torch.int16), stable=True)]
         sends.append(packed)
         counts.append(torch.bincount(o, minlength=P).cpu().tolist())
     recvd = _alltoallv(comm, sends, counts)
@@ -132,8 +134,7 @@ def build_shards(pairs: Sequence, comm):
         dense = back[k][inv[k]]
         offs = torch.zeros(verts.numel() + 1, dtype=torch.int64, device=dev)
         offs[1:] = torch.cumsum(deg, 0)
-        out.append((offs.cpu().numpy().astype(np.uint64), dense.cpu().numpy().astype(np.uint32),
-                    verts.cpu().numpy().astype(np.uint64)))
+        out.append((offs, dense.to(torch.int32), verts))
     n = int(sum(counts_v))
     bounds = np.concatenate([base, [n]]).astype(np.uint64)
     return n, bounds, out
@@ -152,58 +153,62 @@ def coreness_from_pairs_distributed(u, v, approx=None):
 
 
 # ------------------------------------------------------------------ per-shard get_core
+def _dev(x, dev, dtype):
+    import torch
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=dtype)
+    return torch.as_tensor(np.asarray(x).astype(np.int64), device=dev).to(dtype)
+
+
 def shard_get_core(comm, bounds, rows, labels, k: int):
     """get_core (core.cpp:133-140 -> induced_subgraph, graph.hpp:50-80) on the
     shards: each rank keeps its vertices with label >= k; new dense ids =
     exclusive scan of the kept counts over ranks (old order preserved); the
-    old->new map is all-gathered (4 B per vertex) so every rank renames its
+    old->new map is all-gathered (one id per vertex) so every rank renames its
     kept arcs locally.  rows / labels: per local shard (offs, adj, orig) and
-    labels (numpy or tensors).  Returns (n', bounds', rows', labels')."""
+    labels (tensors or numpy).  Returns (n', bounds', rows', labels') with
+    rows' / labels' tensors on the communicator's device."""
     import torch
     dev = comm.device
-    keeps, maps_local = [], []
-    kept = [int((torch.as_tensor(np.asarray(l, np.int64)) >= k).sum()) for l in labels]
-    counts = comm.allgather_counts(kept)
+    labs = [_dev(l, dev, torch.int64) for l in labels]
+    keeps = [l >= k for l in labs]
+    counts = comm.allgather_counts([int(kp.sum()) for kp in keeps])
     base = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
-    for (r, lab) in zip(comm.shards(), labels):
-        keep = torch.as_tensor(np.asarray(lab, np.int64), device=dev) >= k
+    maps_local = []
+    for r, keep in zip(comm.shards(), keeps):
         new = torch.cumsum(keep.to(torch.int64), 0) - 1 + int(base[r])
-        keeps.append(keep)
         maps_local.append(torch.where(keep, new, torch.full_like(new, -1)))
     full = torch.cat(comm.allgatherv(maps_local))
     out_rows, out_labels = [], []
-    for (offs, adj, orig), lab, keep in zip(rows, labels, keeps):
-        offs = torch.as_tensor(np.asarray(offs, np.int64), device=dev)
-        adj = torch.as_tensor(np.asarray(adj, np.int64), device=dev)
+    for (offs, adj, orig), lab, keep in zip(rows, labs, keeps):
+        offs = _dev(offs, dev, torch.int64)
+        adj = _dev(adj, dev, torch.int64) & 0xFFFFFFFF
         nl = offs.numel() - 1
-        row = torch.repeat_interleave(torch.arange(nl, device=dev), offs[1:] - offs[:-1])
-        nadj = full[adj] if adj.numel() else adj
+        row = torch.repeat_interleave(torch.arange(nl, device=dev), offs[1:] - offs[:-1],
+                                      output_size=adj.numel())
+        nadj = full[adj]
         ka = keep[row] & (nadj >= 0)
         deg = torch.bincount(row[ka], minlength=nl)[keep]
         noffs = torch.zeros(deg.numel() + 1, dtype=torch.int64, device=dev)
         noffs[1:] = torch.cumsum(deg, 0)
-        out_rows.append((noffs.cpu().numpy().astype(np.uint64),
-                         nadj[ka].cpu().numpy().astype(np.uint32),
-                         np.asarray(orig, np.uint64)[keep.cpu().numpy()]))
-        out_labels.append(np.asarray(lab, np.uint32)[keep.cpu().numpy()])
+        out_rows.append((noffs, nadj[ka].to(torch.int32), _dev(orig, dev, torch.int64)[keep]))
+        out_labels.append(lab[keep])
     n2 = int(sum(counts))
     return n2, np.concatenate([base, [n2]]).astype(np.uint64), out_rows, out_labels
 
 
 def gather_rows(comm, rows, labels):
-    """All ranks get the whole (core) CSR: offs, adj, orig, labels (numpy)."""
+    """All ranks get the whole (core) CSR as device tensors: offs (int64),
+    adj (int32 holding uint32 bits), orig (int64), labels (int64)."""
     import torch
     dev = comm.device
-
-    def gat(arrs):
-        ts = [torch.as_tensor(np.asarray(a, np.int64), device=dev) for a in arrs]
-        return torch.cat(comm.allgatherv(ts)).cpu().numpy()
-
-    deg = gat([np.diff(np.asarray(o, np.int64)) for o, _, _ in rows])
-    offs = np.zeros(len(deg) + 1, np.uint64)
-    offs[1:] = np.cumsum(deg)
-    return (offs, gat([a for _, a, _ in rows]).astype(np.uint32),
-            gat([o for _, _, o in rows]).astype(np.uint64), gat(labels).astype(np.uint32))
+    deg = torch.cat(comm.allgatherv([_dev(o, dev, torch.int64).diff() for o, _, _ in rows]))
+    offs = torch.zeros(deg.numel() + 1, dtype=torch.int64, device=dev)
+    offs[1:] = torch.cumsum(deg, 0)
+    adj = torch.cat(comm.allgatherv([_dev(a, dev, torch.int32) for _, a, _ in rows]))
+    orig = torch.cat(comm.allgatherv([_dev(o, dev, torch.int64) for _, _, o in rows]))
+    lab = torch.cat(comm.allgatherv([_dev(l, dev, torch.int64) for l in labels]))
+    return offs, adj, orig, lab
 
 
 def prune_distributed(pairs, comm, make_shard, cfg):
@@ -242,4 +247,5 @@ def run_distributed(u, v, cfg=None):
     comm = TorchComm(torch.device("cuda", torch.cuda.current_device()))
     offs, adj, orig, lab, kmax, rounds = prune_distributed([(u, v)], comm, CudaShard.from_rows,
                                                            cfg)
-    return run_pruned(Graph.from_csr(offs, adj, orig), lab, kmax, rounds, cfg)
+    return run_pruned(Graph.from_device_csr(offs, adj, orig), lab.cpu().numpy(), kmax, rounds,
+                      cfg)

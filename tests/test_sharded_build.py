@@ -47,13 +47,22 @@ def _split(u, v, P, skew=False):
              torch.from_numpy(np.asarray(v[cuts[i]:cuts[i + 1]], np.int64))) for i in range(P)]
 
 
+def _np(t, dtype):
+    """tensor (any device) -> numpy; ids are int32/int64 holding unsigned values."""
+    a = t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+    if dtype == np.uint32:
+        return (a.astype(np.int64) & 0xFFFFFFFF).astype(np.uint32)
+    return a.astype(dtype)
+
+
 def _assemble(sh):
     base, offs = 0, [np.zeros(1, np.uint64)]
     for o, _, _ in sh:
+        o = _np(o, np.uint64)
         offs.append(o[1:] + np.uint64(base))
         base += int(o[-1])
-    return (np.concatenate(offs), np.concatenate([s[1] for s in sh]),
-            np.concatenate([s[2] for s in sh]))
+    return (np.concatenate(offs), np.concatenate([_np(s[1], np.uint32) for s in sh]),
+            np.concatenate([_np(s[2], np.uint64) for s in sh]))
 
 
 def _check_csr(g, n, bounds, sh):
@@ -84,7 +93,7 @@ def test_build_balances_arcs(orc):
     g = orc.build(u, v)
     P = 4
     n, bounds, sh = build_shards(_split(u, v, P), LocalComm(P, "cpu"))
-    arcs = np.array([int(o[-1]) for o, _, _ in sh])
+    arcs = np.array([int(_np(o, np.uint64)[-1]) for o, _, _ in sh])
     assert arcs.sum() == int(g.offs[-1])
     # bucket-granular split: within 25% of the ideal share on RMAT-14
     assert arcs.max() <= 1.25 * arcs.sum() / P
@@ -182,6 +191,8 @@ def _expected_core(orc, g, pruning, c_num=3, c_den=2):
 
 def _check_core(orc, g, pruning, got):
     offs, adj, orig, lab, kmax, rounds = got
+    offs, adj, orig, lab = (_np(offs, np.uint64), _np(adj, np.uint32), _np(orig, np.uint64),
+                            _np(lab, np.uint32))
     core, elab, ek, er = _expected_core(orc, g, pruning)
     np.testing.assert_array_equal(offs, core.offs)
     np.testing.assert_array_equal(adj, core.adj)
@@ -263,7 +274,8 @@ def test_run_pruned_matches_run(orc, dg, P):
                 pairs = [(a.cuda(), b.cuda()) for a, b in _split(u, v, P)]
                 offs, adj, orig, lab, kmax, rounds = prune_distributed(
                     pairs, LocalComm(P), CudaShard.from_rows, cfg)
-                got = dg.run_pruned(dg.Graph.from_csr(offs, adj, orig), lab, kmax, rounds, cfg)
+                got = dg.run_pruned(dg.Graph.from_device_csr(offs, adj, orig),
+                                    lab.cpu().numpy(), kmax, rounds, cfg)
                 want = dg.run(g, cfg)
                 ref = orc.run(hg, ORC(algorithm=algorithm, pruning=pruning, iterations=6))
                 assert got.best == want.best
