@@ -515,3 +515,46 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+def _parse_device(dg, raw: bytes, off: int):
+    """dg_parse_edge_list on device text starting `off` bytes into an allocation."""
+    import ctypes as C
+    buf = dg.DeviceBuffer(len(raw) + 16)
+    dg._chk(dg.LIB.dg_memcpy(C.c_void_p(buf.ptr + off), raw, len(raw), 1))
+    h, bad = C.c_void_p(), C.c_uint64()
+    st = dg.LIB.dg_parse_edge_list(C.cast(C.c_void_p(buf.ptr + off), C.c_char_p), len(raw),
+                                   b"#", 1, C.byref(h), C.byref(bad))
+    return st, (dg.Graph(h) if st == 0 else None), bad.value
+
+
+def test_parse_tiles_long_lines_and_alignment(dg, orc):
+    """Tiled tokeniser edge cases: lines straddling 8 KB tiles at every offset,
+    blank runs and comment lines far longer than the 256-byte halo, empty
+    lines, CRLF, text starting at every 16-byte misalignment; the first bad
+    line after long lines is reported by number."""
+    rng = np.random.default_rng(17)
+    u, v = orc.gen_rmat(12, 20000, 77)
+    lines = []
+    for a, b in zip(u.tolist(), v.tolist()):
+        r = rng.random()
+        if r < 0.02:
+            lines.append("#" + "c" * int(rng.integers(200, 20000)))
+        elif r < 0.04:
+            lines.append("")
+        sep = " " * int(rng.integers(1, 600)) if rng.random() < 0.05 else "\t"
+        lead = " " * int(rng.integers(0, 400)) if rng.random() < 0.03 else ""
+        lines.append(f"{lead}{a}{sep}{b}" + ("\r" if rng.random() < 0.3 else ""))
+    text = "\n".join(lines)  # no final newline
+    raw = text.encode()
+    h = orc.build(u, v)
+    for off in (0, 1, 3, 7, 8, 13, 15):
+        st, g, _ = _parse_device(dg, raw, off)
+        assert st == 0 and same_csr(g, h), off
+    # a bad line after the long ones: its 1-based number
+    bad_at = len(lines) - 5
+    bad_lines = lines[:bad_at] + ["12 x7"] + lines[bad_at:] + ["1 2 3"]
+    raw = "\n".join(bad_lines).encode()
+    for off in (0, 5):
+        st, g, line = _parse_device(dg, raw, off)
+        assert st != 0 and line == bad_at + 1, (off, line)
