@@ -234,6 +234,9 @@ class CudaShard:
     def expand(self, bound: int, label: int, counts: List[int]):
         displs = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
         send = self.torch.empty(max(1, int(sum(counts))), dtype=self.torch.int32, device="cuda")
+        # torch's allocator may hand out a block that pending work on torch's
+        # stream still writes; the library writes it on its own stream
+        self.torch.cuda.synchronize()
         self._chk(self.LIB.dg_shard_expand(self._h, bound, label,
                                            displs.ctypes.data_as(self.u64p),
                                            C.c_void_p(send.data_ptr())))
@@ -242,6 +245,7 @@ class CudaShard:
     def apply(self, recv, bound: int, label: int) -> int:
         x = C.c_uint64()
         ptr = recv.data_ptr() if recv.numel() else 0
+        self.torch.cuda.synchronize()  # recv comes from torch ops (LocalComm) or NCCL
         self._chk(self.LIB.dg_shard_apply(self._h, C.c_void_p(ptr), recv.numel(), bound, label,
                                           C.byref(x)))
         return x.value
