@@ -550,10 +550,11 @@ def synchronize() -> None:
 def _run(g: Graph, cfg: Optional[RunConfig], pruned=None) -> RunResult:
     cfg = cfg or RunConfig()
     res = DgRunResult()
-    cap = 1 << 16
+    # explicit T sizes the trace exactly; else the iteration cap bounds it
+    cap = max(1, cfg.iterations if cfg.iterations else cfg.iteration_cap)
     trace = (DgIterRecord * cap)()
-    wit = np.zeros(max(g.n, 1), np.uint64)
-    fin = np.zeros(max(g.n, 1), np.uint64)
+    wit = np.empty(max(g.n, 1), np.uint64)  # only the returned prefixes are read
+    fin = np.empty(max(g.n, 1), np.uint64)
     c = cfg.to_c()
     if pruned is None:
         _chk(LIB.dg_run(g._h, C.byref(c), C.byref(res), trace, cap, _p(wit, u64p), g.n,
