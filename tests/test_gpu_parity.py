@@ -352,11 +352,13 @@ def test_peel_kernel_modes_agree(dg, orc, golden, mode):
 
 
 @pytest.mark.gpu
-def test_peel_queue_paths(dg, orc):
-    """Candidate-list kernel corner paths against the oracle's batch peel
-    (refine.cpp:20-156): a tie group larger than the member staging (ordered
-    full-scan batch), widely spread loads (frequent window rebases), many
-    large batches (slice removal) and loads whose keys cross the window."""
+@pytest.mark.parametrize("mode", [3, 1, 2])
+def test_peel_queue_paths(dg, orc, mode):
+    """Corner paths against the oracle's batch peel (refine.cpp:20-156), for
+    the candidate-list kernel (mode 3) and the scanning and cluster kernels
+    (modes 1, 2): a tie group larger than the member staging / the CTA (1500
+    members), widely spread loads (frequent window rebases), many large
+    batches (slice removal) and loads whose keys cross the window."""
     rng = np.random.default_rng(7)
     cases = []
     # K_{1500,40}: 1500 vertices tie at key 40 > 1024 staged members
@@ -368,7 +370,7 @@ def test_peel_queue_paths(dg, orc):
     cases.append((gu, gv, rng.integers(0, 64, 4000).astype(np.uint64)))
     ru, rv = orc.gen_rmat(14, 8 << 14, 5)
     cases.append((ru, rv, None))
-    dg.set_peel_mode(3)
+    dg.set_peel_mode(mode)
     try:
         for u, v, loads in cases:
             g = dg.Graph.from_pairs(u, v)
