@@ -99,6 +99,7 @@ struct Smem {
 // staged in shared memory during the min scan (a CTA's overflow spills to a
 // global list), so the usual small jump needs no second pass.
 constexpr uint32_t LW = 16;
+constexpr int LE = 4;  // live-list entries per thread in the level pass
 
 __device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
   s.b_front = ld_relaxed_u64(&acc->front);
@@ -186,6 +187,82 @@ __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const ui
   }
 }
 
+// Level-advance pass over the live list (see k_coreness): min alive degree,
+// compaction into live_out (list order kept), candidates within LW of the
+// bound staged in shared memory (overflow spilled to a.cand).  E contiguous
+// entries per thread: E independent load chains and one CTA scan per
+// E * blockDim entries.
+template <bool BM, int E>
+__device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint32_t* live_in,
+                                           uint32_t* live_out, uint32_t livec, bool implicit,
+                                           uint64_t win, Acc* acc, uint32_t& lmin) {
+  const uint32_t lane = lane_id();
+  const uint64_t tile = uint64_t(blockDim.x) * E;
+  const uint64_t stride = uint64_t(gridDim.x) * tile;
+  for (uint64_t base = uint64_t(blockIdx.x) * tile; base < livec; base += stride) {
+    const uint64_t i0 = base + uint64_t(threadIdx.x) * E;
+    uint32_t v[E], d[E];
+    bool alive[E];
+    if (E == 4 && !implicit && i0 + E <= livec) {
+      const uint4 q = *reinterpret_cast<const uint4*>(live_in + i0);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = w[e & 3];
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        v[e] = implicit ? uint32_t(i0 + e) : (i0 + e < livec ? live_in[i0 + e] : 0u);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      alive[e] = false;
+      d[e] = kUnset;
+      if (i0 + e < livec) {
+        const uint32_t x = v[e];
+        alive[e] = BM ? ((ld_relaxed_u32(&a.alive[x >> 5]) >> (x & 31)) & 1u) != 0
+                      : a.labels[x] == kUnset;
+        if (alive[e]) d[e] = a.deg[x];
+      }
+    }
+    uint32_t c = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      lmin = min(lmin, d[e]);
+      c += alive[e];
+      bool spill = false;
+      if (alive[e] && d[e] <= win) {
+        const uint32_t slot = atomicAdd(&s.cnt, 1u);
+        if (slot < BUF) {
+          const uint64_t o0 = a.offs[v[e]];
+          s.id[slot] = v[e];
+          s.rd[slot] = d[e];
+          s.of[slot] = o0;
+          s.dg[slot] = uint32_t(a.offs[v[e] + 1] - o0);
+        } else {
+          spill = true;
+        }
+      }
+      // overflow -> global candidate list, warp-aggregated
+      const uint32_t cm = __ballot_sync(~0u, spill);
+      if (cm) {
+        unsigned long long cb = 0;
+        if (lane == 0) cb = atomicAdd(&acc->ccnt, (unsigned long long)__popc(cm));
+        cb = __shfl_sync(~0u, cb, 0);
+        if (spill) a.cand[cb + __popc(cm & ((1u << lane) - 1u))] = v[e];
+      }
+    }
+    uint32_t totL;
+    const uint32_t exL = block_excl_scan<uint32_t>(c, s.ws32, &totL);
+    if (threadIdx.x == 0 && totL) s.baseL = atomicAdd(&acc->live, (unsigned long long)totL);
+    __syncthreads();
+    uint64_t o = s.baseL + exL;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (alive[e]) live_out[o++] = v[e];
+    __syncthreads();  // s.baseL / ws32 reuse
+  }
+}
+
 // 64-bit warp shuffle
 __device__ __forceinline__ uint64_t shfl64(uint64_t x, uint32_t src) {
   return __shfl_sync(~0u, x, src);
@@ -241,49 +318,11 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       if (threadIdx.x == 0) s.cnt = 0;
       __syncthreads();
       uint32_t lmin = kUnset;
-      {
-        const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-        for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < livec; base += stride) {
-          const uint64_t i = base + threadIdx.x;
-          uint32_t v = 0, d = kUnset;
-          bool alive = false;
-          if (i < livec) {
-            v = implicit ? uint32_t(i) : live_in[i];
-            alive = BM ? ((ld_relaxed_u32(&a.alive[v >> 5]) >> (v & 31)) & 1u) != 0
-                       : a.labels[v] == kUnset;
-            if (alive) d = a.deg[v];
-          }
-          lmin = min(lmin, d);
-          bool spill = false;
-          if (alive && d <= win) {
-            const uint32_t slot = atomicAdd(&s.cnt, 1u);
-            if (slot < BUF) {
-              const uint64_t o0 = a.offs[v];
-              s.id[slot] = v;
-              s.rd[slot] = d;
-              s.of[slot] = o0;
-              s.dg[slot] = uint32_t(a.offs[v + 1] - o0);
-            } else {
-              spill = true;
-            }
-          }
-          {  // overflow -> global candidate list, warp-aggregated
-            const uint32_t cm = __ballot_sync(~0u, spill);
-            if (cm) {
-              unsigned long long cb = 0;
-              if (lane == 0) cb = atomicAdd(&acc->ccnt, (unsigned long long)__popc(cm));
-              cb = __shfl_sync(~0u, cb, 0);
-              if (spill) a.cand[cb + __popc(cm & ((1u << lane) - 1u))] = v;
-            }
-          }
-          uint32_t totL;
-          const uint32_t exL = block_excl_scan<uint32_t>(alive ? 1u : 0u, s.ws32, &totL);
-          if (threadIdx.x == 0 && totL) s.baseL = atomicAdd(&acc->live, (unsigned long long)totL);
-          __syncthreads();
-          if (alive) live_out[s.baseL + exL] = v;
-          __syncthreads();  // s.baseL / ws32 reuse
-        }
-      }
+      // wide tiles only while the list fills the grid LE times over
+      if (livec >= uint64_t(gridDim.x) * blockDim.x * LE)
+        level_pass<BM, LE>(a, s, live_in, live_out, livec, implicit, win, acc, lmin);
+      else
+        level_pass<BM, 1>(a, s, live_in, live_out, livec, implicit, win, acc, lmin);
       lmin = __reduce_min_sync(~0u, lmin);
       if (lane == 0) s.ws32[threadIdx.x >> 5] = lmin;
       __syncthreads();

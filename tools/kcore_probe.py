@@ -1,4 +1,4 @@
-"""k-core phase split: python tools/kcore_probe.py [scale]"""
+"""k-core phase split: python tools/kcore_probe.py [scale | bench config name]"""
 import ctypes as C
 import os
 import sys
@@ -8,8 +8,14 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2311_04333_b200 as dg  # noqa: E402
 
-scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
-g = dg.Graph.generate_rmat(scale, 16 << scale, scale)
+arg = sys.argv[1] if len(sys.argv) > 1 else "22"
+if arg.isdigit():
+    scale = int(arg)
+    g = dg.Graph.generate_rmat(scale, 16 << scale, scale)
+else:
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench  # noqa: E402
+    g = bench.device_graph(dg, bench.CONFIGS[arg])
 for _ in range(2):
     r = dg.run(g, dg.RunConfig(iterations=1))
 p = np.zeros(8 + 3 * 4096, np.uint64)
