@@ -560,3 +560,23 @@ def test_parse_tiles_long_lines_and_alignment(dg, orc):
     for off in (0, 5):
         st, g, line = _parse_device(dg, raw, off)
         assert st != 0 and line == bad_at + 1, (off, line)
+
+
+@pytest.mark.gpu
+def test_coreness_near_list_paths(dg, orc):
+    """k_coreness keeps a near list (alive vertices with degree <= thr) so
+    most level advances scan it instead of the live list; rebuilds, large
+    jumps inside it, and approximate phases jumping past thr all must give
+    the reference's labels / kmax / peel_rounds (core.cpp:89-119)."""
+    graphs = [orc.gen_rmat(18, 16 << 18, 181), orc.gen_chung_lu(200000, 1500000, 9),
+              orc.gen_er_planted(60000, 400000, 200, 4)]
+    for u, v in graphs:
+        h = orc.build(u, v)
+        g = dg.Graph.from_pairs(u, v)
+        d = dg.exact_coreness(g)
+        lab, k, r = orc.coreness(h)
+        assert np.array_equal(d.labels, lab) and (d.kmax, d.peel_rounds) == (k, r)
+        for cn, cd in ((3, 2), (2, 1), (11, 10), (5, 1)):
+            a = dg.approx_coreness(g, cn, cd)
+            al, ak, ar = orc.coreness(h, True, cn, cd)
+            assert np.array_equal(a.labels, al) and (a.kmax, a.peel_rounds) == (ak, ar), (cn, cd)
