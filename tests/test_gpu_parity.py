@@ -563,11 +563,11 @@ def test_parse_tiles_long_lines_and_alignment(dg, orc):
 
 
 @pytest.mark.gpu
-def test_coreness_near_list_paths(dg, orc):
-    """k_coreness keeps a near list (alive vertices with degree <= thr) so
-    most level advances scan it instead of the live list; rebuilds, large
-    jumps inside it, and approximate phases jumping past thr all must give
-    the reference's labels / kmax / peel_rounds (core.cpp:89-119)."""
+def test_coreness_level_advance_paths(dg, orc):
+    """Level advances of k_coreness on three graph families: wide (4 entries
+    per thread) and narrow live-list passes, jumps inside and beyond the
+    staged window, approximate phases for several c -- labels / kmax /
+    peel_rounds equal the reference's (core.cpp:89-119)."""
     graphs = [orc.gen_rmat(18, 16 << 18, 181), orc.gen_chung_lu(200000, 1500000, 9),
               orc.gen_er_planted(60000, 400000, 200, 4)]
     for u, v in graphs:
