@@ -237,6 +237,24 @@ dg_status dg_shard_apply(dg_shard* s, const uint32_t* d_recv /* device */, uint6
                          uint32_t bound, uint32_t label, uint64_t* nnext);
 dg_status dg_shard_labels(const dg_shard* s, uint32_t* labels /* hi - lo entries */);
 
+/* Peer mode: the fused form of the round above.  Each shard's decrement
+ * targets (degrees, labels, two frontier queues + counters) live in one
+ * device allocation that every other rank maps -- by CUDA IPC
+ * (dg_shard_ipc_handle on the owner, dg_shard_peer_open on the others: NVLink
+ * peer memory on one node) or directly for shards of one process
+ * (dg_shard_peer_link).  dg_shard_expand_peer then decrements every
+ * neighbour AT ITS OWNER with system-scope atomics and appends crossings to
+ * the owner's next queue, returning how many crossings this shard produced;
+ * after an all-reduce of those counts (the round barrier) dg_shard_finish_round
+ * makes the owner's queue its frontier.  Level advances are unchanged
+ * (dg_shard_min_alive / dg_shard_collect).  Every rank must be opened or
+ * linked (its own entry is implicit); at most 64 shards. */
+dg_status dg_shard_ipc_handle(const dg_shard* s, void* handle /* 64 bytes out */);
+dg_status dg_shard_peer_open(dg_shard* s, uint32_t rank, const void* handle /* 64 bytes */);
+dg_status dg_shard_peer_link(dg_shard* s, uint32_t rank, const dg_shard* other);
+dg_status dg_shard_expand_peer(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* produced);
+dg_status dg_shard_finish_round(dg_shard* s, uint64_t* nnext);
+
 /* ------------------------------------------------------------ synthetic inputs */
 
 /* Seeded counter-based generators (bit-identical to oracle/dg_oracle.c).

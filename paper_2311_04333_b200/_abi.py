@@ -89,6 +89,11 @@ PROTOTYPES = {
     "dg_shard_expand": (C.c_int, [GP, C.c_uint32, C.c_uint32, u64p, C.c_void_p]),
     "dg_shard_apply": (C.c_int, [GP, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, u64p]),
     "dg_shard_labels": (C.c_int, [GP, u32p]),
+    "dg_shard_ipc_handle": (C.c_int, [GP, C.c_void_p]),
+    "dg_shard_peer_open": (C.c_int, [GP, C.c_uint32, C.c_void_p]),
+    "dg_shard_peer_link": (C.c_int, [GP, C.c_uint32, GP]),
+    "dg_shard_expand_peer": (C.c_int, [GP, C.c_uint32, C.c_uint32, u64p]),
+    "dg_shard_finish_round": (C.c_int, [GP, u64p]),
     "dg_gen_rmat": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                               C.c_int]),
     "dg_gen_chung_lu": (C.c_int, [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, C.c_void_p,

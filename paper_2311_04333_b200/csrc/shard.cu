@@ -6,20 +6,48 @@
 // exchange; received decrements are applied with the same crossing rule.
 // The round / level protocol (frontier-size sum, min-degree agreement,
 // decrement all-to-all) lives in paper_2311_04333_b200/sharded.py over NCCL.
+//
+// Peer mode (fused compute + exchange): the state the owners' decrements
+// touch -- degrees, labels, the two frontier queues and their counters -- is
+// ONE cudaMalloc'd block per shard, exported by CUDA IPC (or shared directly
+// between shards of one process).  dg_shard_expand_peer decrements every
+// neighbour at its owner with system-scope atomics over NVLink peer memory,
+// and the decrement that crosses the bound labels the vertex and appends it
+// to the owner's next-frontier queue: no send buffers, no all-to-all, one
+// all-reduce (the produced crossings) per round.
+#include <cstring>
 #include <vector>
 
 #include "internal.cuh"
+
+// device view of one shard's peer block
+struct PeerView {
+  uint32_t* deg;
+  uint32_t* labels;
+  uint32_t* q[2];               // frontier queues (round parity)
+  unsigned long long* ctr;      // [2] queue counters
+};
 
 struct dg_shard {
   uint64_t n = 0;  // global vertex count
   uint64_t lo = 0, hi = 0;
   dgb::DevBuf<uint64_t> offs;  // the rank's own rows: local offsets, n_local + 1
   dgb::DevBuf<uint32_t> adj;   // neighbour ids (global dense ids)
-  dgb::DevBuf<uint32_t> deg, labels, front, next;
+  void* block = nullptr;       // peer-visible state (cudaMalloc: IPC-exportable)
+  PeerView own{};
+  uint32_t cur = 0;            // queue holding the current frontier
   dgb::DevBuf<unsigned long long> cnt;  // [0] next size, [1] min, [2..] per-rank counts
   uint64_t nfront = 0;
   dgb::DevBuf<uint64_t> bounds;  // rank boundaries (P + 1)
   uint32_t P = 0;
+  std::vector<PeerView> peers;   // per rank (own entry included)
+  std::vector<void*> opened;     // IPC mappings to close
+  dgb::DevBuf<PeerView> d_peers;
+  bool peers_ready = false;
+  ~dg_shard() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    if (block) cudaFree(block);
+  }
 };
 
 namespace dgb {
@@ -115,6 +143,48 @@ __global__ void k_sh_apply(const uint32_t* recv, uint64_t nrecv, uint64_t lo, ui
     dec_local(deg, labels, uint32_t(recv[i] - lo), bound, label, next, cnt);
 }
 
+// Peer mode: warp per frontier vertex; every neighbour is decremented at its
+// owner (peers[r] maps rank r's block: NVLink peer memory, or this GPU) with
+// system-scope atomics; the crossing decrement labels the vertex and appends
+// it to the owner's queue qn.  `produced` counts this shard's crossings (the
+// per-round all-reduce sums them).
+constexpr uint32_t kMaxPeers = 64;
+
+__global__ void k_sh_expand_peer(const uint64_t* offs, const uint32_t* adj, const uint32_t* front,
+                                 uint64_t nfront, const uint64_t* bounds, uint32_t P,
+                                 const PeerView* peers, uint32_t bound, uint32_t label,
+                                 uint32_t qn, unsigned long long* produced) {
+  __shared__ uint64_t sb[kMaxPeers + 1];
+  __shared__ PeerView sp[kMaxPeers];
+  for (uint32_t i = threadIdx.x; i <= P; i += blockDim.x) sb[i] = bounds[i];
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sp[i] = peers[i];
+  __syncthreads();
+  uint32_t made = 0;
+  const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t f = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; f < nfront;
+       f += warps) {
+    const uint64_t v = front[f];  // local row
+    for (uint64_t p = offs[v] + lane_id(); p < offs[v + 1]; p += 32) {
+      const uint64_t u = adj[p];
+      uint32_t r = 0;
+      while (r + 1 < P && u >= sb[r + 1]) ++r;
+      const PeerView& pv = sp[r];
+      const uint32_t i = uint32_t(u - sb[r]);
+      // a stale (higher) degree only costs an extra atomic: degrees only fall
+      if (pv.deg[i] <= bound) continue;
+      if (atomicSub_system(&pv.deg[i], 1u) == bound + 1) {
+        pv.labels[i] = label;
+        const unsigned long long slot = atomicAdd_system(&pv.ctr[qn], 1ULL);
+        pv.q[qn][slot] = i;
+        ++made;
+      }
+    }
+  }
+  __threadfence_system();  // peer stores visible before the round's barrier
+  made = __reduce_add_sync(~0u, made);
+  if (lane_id() == 0 && made) atomicAdd(produced, (unsigned long long)made);
+}
+
 }  // namespace
 }  // namespace dgb
 
@@ -134,18 +204,32 @@ using namespace dgb;
 extern "C" {
 
 // common tail: state arrays, degree init
+// block layout: ctr u64[2] | deg | labels | q0 | q1 (u32[nl] each)
+static size_t block_bytes(uint64_t nl) { return 16 + 16 * (nl ? nl : 1); }
+static PeerView block_view(void* block, uint64_t nl) {
+  char* b = static_cast<char*>(block);
+  const uint64_t w = nl ? nl : 1;
+  PeerView v;
+  v.ctr = reinterpret_cast<unsigned long long*>(b);
+  v.deg = reinterpret_cast<uint32_t*>(b + 16);
+  v.labels = v.deg + w;
+  v.q[0] = v.labels + w;
+  v.q[1] = v.q[0] + w;
+  return v;
+}
+
 static void shard_init_state(dg_shard* s, const uint64_t* bounds, uint32_t P) {
   const uint64_t nl = s->hi - s->lo;
-  s->deg.alloc(nl);
-  s->labels.alloc(nl);
-  s->front.alloc(nl);
-  s->next.alloc(nl);
+  DG_CUDA(cudaMalloc(&s->block, block_bytes(nl)));
+  s->own = block_view(s->block, nl);
+  DG_CUDA(cudaMemsetAsync(s->own.ctr, 0, 16, stream()));
+  s->peers.assign(P, PeerView{});
   s->cnt.alloc(2 + P);
   s->bounds.alloc(P + 1);
   h2d(s->bounds.get(), bounds, P + 1);
   if (nl) {
-    k_sh_init<<<grid_for(nl, 256), 256, 0, stream()>>>(s->offs.get(), nl, s->deg.get(),
-                                                        s->labels.get());
+    k_sh_init<<<grid_for(nl, 256), 256, 0, stream()>>>(s->offs.get(), nl, s->own.deg,
+                                                        s->own.labels);
     DG_CHECK_LAUNCH();
   }
   stream_sync();
@@ -183,6 +267,7 @@ dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P,
     DG_CUDA(cudaMemcpyAsync(s->adj.get(), g->adj.get() + a0, (a1 - a0) * 4,
                             cudaMemcpyDeviceToDevice, stream()));
   shard_init_state(s.get(), bounds, P);
+  s->peers[rank] = s->own;
   *out = s.release();
   SH_END
 }
@@ -223,6 +308,7 @@ dg_status dg_shard_create_rows(uint64_t n, const uint64_t* bounds, uint32_t P, u
                             stream()));
   }
   shard_init_state(s.get(), bounds, P);
+  s->peers[rank] = s->own;
   *out = s.release();
   SH_END
 }
@@ -240,7 +326,7 @@ dg_status dg_shard_min_alive(dg_shard* s, uint32_t* out) {
   unsigned long long init = kUnset;
   h2d(s->cnt.get() + 1, &init, 1);
   if (nl) {
-    k_sh_min<<<grid_for(nl, 256), 256, 0, stream()>>>(s->deg.get(), s->labels.get(), nl,
+    k_sh_min<<<grid_for(nl, 256), 256, 0, stream()>>>(s->own.deg, s->own.labels, nl,
                                                        s->cnt.get() + 1);
     DG_CHECK_LAUNCH();
   }
@@ -253,8 +339,8 @@ dg_status dg_shard_collect(dg_shard* s, uint32_t bound, uint32_t label, uint64_t
   const uint64_t nl = s->hi - s->lo;
   s->cnt.zero();
   if (nl) {
-    k_sh_collect<<<grid_for(nl, 256), 256, 0, stream()>>>(s->deg.get(), s->labels.get(), nl,
-                                                           bound, label, s->front.get(),
+    k_sh_collect<<<grid_for(nl, 256), 256, 0, stream()>>>(s->own.deg, s->own.labels, nl,
+                                                           bound, label, s->own.q[s->cur],
                                                            s->cnt.get());
     DG_CHECK_LAUNCH();
   }
@@ -268,8 +354,8 @@ dg_status dg_shard_count_remote(dg_shard* s, uint64_t* counts) {
   s->cnt.zero();
   if (s->nfront) {
     k_sh_expand<false><<<grid_for(s->nfront * 32, 256), 256, 0, stream()>>>(
-        s->offs.get(), s->adj.get(), s->lo, s->hi, s->front.get(), s->nfront,
-        s->bounds.get(), s->P, s->deg.get(), s->labels.get(), 0, 0, nullptr, s->cnt.get(),
+        s->offs.get(), s->adj.get(), s->lo, s->hi, s->own.q[s->cur], s->nfront,
+        s->bounds.get(), s->P, s->own.deg, s->own.labels, 0, 0, nullptr, s->cnt.get(),
         nullptr, nullptr);
     DG_CHECK_LAUNCH();
   }
@@ -289,8 +375,8 @@ dg_status dg_shard_expand(dg_shard* s, uint32_t bound, uint32_t label, const uin
   s->cnt.zero();
   if (s->nfront) {
     k_sh_expand<true><<<grid_for(s->nfront * 32, 256), 256, 0, stream()>>>(
-        s->offs.get(), s->adj.get(), s->lo, s->hi, s->front.get(), s->nfront,
-        s->bounds.get(), s->P, s->deg.get(), s->labels.get(), bound, label, s->next.get(),
+        s->offs.get(), s->adj.get(), s->lo, s->hi, s->own.q[s->cur], s->nfront,
+        s->bounds.get(), s->P, s->own.deg, s->own.labels, bound, label, s->own.q[s->cur ^ 1],
         s->cnt.get(), cur.get(), d_send);
     DG_CHECK_LAUNCH();
   }
@@ -302,20 +388,94 @@ dg_status dg_shard_apply(dg_shard* s, const uint32_t* d_recv, uint64_t nrecv, ui
                          uint32_t label, uint64_t* nnext) {
   SH_TRY
   if (nrecv) {
-    k_sh_apply<<<grid_for(nrecv, 256), 256, 0, stream()>>>(d_recv, nrecv, s->lo, s->deg.get(),
-                                                           s->labels.get(), bound, label,
-                                                           s->next.get(), s->cnt.get());
+    k_sh_apply<<<grid_for(nrecv, 256), 256, 0, stream()>>>(d_recv, nrecv, s->lo, s->own.deg,
+                                                           s->own.labels, bound, label,
+                                                           s->own.q[s->cur ^ 1], s->cnt.get());
     DG_CHECK_LAUNCH();
   }
   s->nfront = read_scalar(s->cnt.get());
-  std::swap(s->front, s->next);
+  s->cur ^= 1;
+  *nnext = s->nfront;
+  SH_END
+}
+
+// ---- peer mode
+static void peer_set(dg_shard* s, uint32_t rank, void* block) {
+  if (rank >= s->P) throw DgError(DG_E_PARAM, "peer rank out of range");
+  std::vector<uint64_t> b(s->P + 1);
+  d2h(b.data(), s->bounds.get(), s->P + 1);
+  stream_sync();
+  s->peers[rank] = block_view(block, b[rank + 1] - b[rank]);
+  s->peers_ready = false;
+}
+
+dg_status dg_shard_ipc_handle(const dg_shard* s, void* handle) {
+  SH_TRY
+  if (!s || !handle) throw DgError(DG_E_PARAM, "null argument");
+  cudaIpcMemHandle_t h;
+  DG_CUDA(cudaIpcGetMemHandle(&h, s->block));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle, &h, sizeof h);
+  SH_END
+}
+
+dg_status dg_shard_peer_open(dg_shard* s, uint32_t rank, const void* handle) {
+  SH_TRY
+  if (!s || !handle) throw DgError(DG_E_PARAM, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  void* p = nullptr;
+  DG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  s->opened.push_back(p);
+  peer_set(s, rank, p);
+  SH_END
+}
+
+dg_status dg_shard_peer_link(dg_shard* s, uint32_t rank, const dg_shard* other) {
+  SH_TRY
+  if (!s || !other) throw DgError(DG_E_PARAM, "null argument");
+  if (other->P != s->P || other->n != s->n) throw DgError(DG_E_PARAM, "shards of different graphs");
+  peer_set(s, rank, other->block);
+  SH_END
+}
+
+dg_status dg_shard_expand_peer(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* produced) {
+  SH_TRY
+  if (!s || !produced) throw DgError(DG_E_PARAM, "null argument");
+  if (s->P > kMaxPeers) throw DgError(DG_E_PARAM, "peer mode supports at most 64 shards");
+  if (!s->peers_ready) {
+    for (const PeerView& v : s->peers)
+      if (!v.deg) throw DgError(DG_E_PARAM, "peer mode needs every rank linked or opened");
+    s->d_peers.alloc(s->P);
+    h2d(s->d_peers.get(), s->peers.data(), s->P);
+    s->peers_ready = true;
+  }
+  // the current queue's counter restarts: remote ranks append into this
+  // queue only in the next round, after the round barrier
+  DG_CUDA(cudaMemsetAsync(s->own.ctr + s->cur, 0, 8, stream()));
+  s->cnt.zero();
+  if (s->nfront) {
+    k_sh_expand_peer<<<grid_for(s->nfront * 32, 256), 256, 0, stream()>>>(
+        s->offs.get(), s->adj.get(), s->own.q[s->cur], s->nfront, s->bounds.get(), s->P,
+        s->d_peers.get(), bound, label, s->cur ^ 1, s->cnt.get());
+    DG_CHECK_LAUNCH();
+  }
+  *produced = read_scalar(s->cnt.get());
+  SH_END
+}
+
+dg_status dg_shard_finish_round(dg_shard* s, uint64_t* nnext) {
+  SH_TRY
+  if (!s || !nnext) throw DgError(DG_E_PARAM, "null argument");
+  s->nfront = read_scalar(s->own.ctr + (s->cur ^ 1));
+  s->cur ^= 1;
   *nnext = s->nfront;
   SH_END
 }
 
 dg_status dg_shard_labels(const dg_shard* s, uint32_t* labels) {
   SH_TRY
-  d2h(labels, s->labels.get(), s->hi - s->lo);
+  d2h(labels, s->own.labels, s->hi - s->lo);
   stream_sync();
   SH_END
 }

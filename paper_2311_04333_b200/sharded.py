@@ -32,7 +32,7 @@ from typing import List, Sequence
 import numpy as np
 
 __all__ = ["partition", "TorchComm", "LocalComm", "CudaShard", "sharded_coreness",
-           "coreness_local_shards", "coreness_distributed"]
+           "coreness_local_shards", "coreness_distributed", "link_local", "link_ipc"]
 
 
 def partition(offs: np.ndarray, P: int) -> np.ndarray:
@@ -250,6 +250,29 @@ class CudaShard:
                                           C.byref(x)))
         return x.value
 
+    # -- peer mode (fused decrement exchange over peer memory, see dg_b200.h)
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_ubyte * 64)()
+        self._chk(self.LIB.dg_shard_ipc_handle(self._h, buf))
+        return bytes(buf)
+
+    def peer_open(self, rank: int, handle: bytes):
+        buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+        self._chk(self.LIB.dg_shard_peer_open(self._h, rank, buf))
+
+    def peer_link(self, rank: int, other: "CudaShard"):
+        self._chk(self.LIB.dg_shard_peer_link(self._h, rank, other._h))
+
+    def expand_peer(self, bound: int, label: int) -> int:
+        x = C.c_uint64()
+        self._chk(self.LIB.dg_shard_expand_peer(self._h, bound, label, C.byref(x)))
+        return x.value
+
+    def finish_round(self) -> int:
+        x = C.c_uint64()
+        self._chk(self.LIB.dg_shard_finish_round(self._h, C.byref(x)))
+        return x.value
+
     def labels(self) -> np.ndarray:
         out = np.zeros(max(1, self.n_local), np.uint32)
         self._chk(self.LIB.dg_shard_labels(self._h, out.ctypes.data_as(self.u32p)))
@@ -260,11 +283,31 @@ class CudaShard:
 UNSET = 0xFFFFFFFF
 
 
-def sharded_coreness(shards: List, comm, n_global: int, approx=None):
+def link_local(shards: List):
+    """Peer mode for shards of one process: map every shard's state into the others."""
+    for s in shards:
+        for r, o in enumerate(shards):
+            if o is not s:
+                s.peer_link(r, o)
+
+
+def link_ipc(shard, comm):
+    """Peer mode across processes: all-gather the CUDA IPC handles of the
+    shards' state blocks and map the others' (NVLink peer memory)."""
+    handles = comm.allgather(shard.ipc_handle())
+    for r, h in enumerate(handles):
+        if r != comm.rank:
+            shard.peer_open(r, h)
+
+
+def sharded_coreness(shards: List, comm, n_global: int, approx=None, peer: bool = False):
     """Coreness over the shards held by this process (core.cpp:89-119).
 
     approx=None is exact_coreness; approx=(c_num, c_den) is approx_coreness
     with geometric phases t_{i+1} = max(t_i + 1, ceil(c * t_i)).
+    peer=True runs the fused rounds (dg_shard_expand_peer: decrements applied
+    at the owners through peer memory, one all-reduce per round) on shards
+    linked by link_local / link_ipc.
     Returns (labels of the local shards in order, kmax, peel_rounds).  Every
     rank executes the same control flow (all decisions come from collectives).
     """
@@ -304,6 +347,11 @@ def sharded_coreness(shards: List, comm, n_global: int, approx=None):
         rounds += 1
         kmax = max(kmax, label)
         remaining -= total
+        if peer:
+            produced = [s.expand_peer(bound, label) for s in shards]
+            comm.allreduce_sum(sum(produced))  # the round barrier
+            nfront = [s.finish_round() for s in shards]
+            continue
         counts = [s.count_remote() for s in shards]
         recv_counts = comm.alltoall_counts(counts)
         sends = [s.expand(bound, label, c) for s, c in zip(shards, counts)]
@@ -320,19 +368,25 @@ def _decomposition(labels, kmax, rounds, approx):
                              c_den=1 if approx is None else approx[1])
 
 
-def coreness_local_shards(g, P: int, approx=None):
+def coreness_local_shards(g, P: int, approx=None, peer: bool = False):
     """All P range shards of `g` on this GPU (validates the shard kernels)."""
     bounds = partition(g.offs, P)
     shards = [CudaShard(g, bounds, r) for r in range(P)]
-    labs, kmax, rounds = sharded_coreness(shards, LocalComm(P), g.n, approx)
+    if peer:
+        link_local(shards)
+    labs, kmax, rounds = sharded_coreness(shards, LocalComm(P), g.n, approx, peer)
     return _decomposition(np.concatenate(labs), kmax, rounds, approx)
 
 
-def coreness_distributed(g, approx=None):
-    """One range shard per torch.distributed rank (NCCL); every rank gets all labels."""
+def coreness_distributed(g, approx=None, peer: bool = True):
+    """One range shard per torch.distributed rank (NCCL); every rank gets all
+    labels.  peer=True maps the other ranks' shard state by CUDA IPC (one
+    node, NVLink) and runs the fused rounds."""
     import torch
     comm = TorchComm(torch.device("cuda", torch.cuda.current_device()))
     bounds = partition(g.offs, comm.P)
     shard = CudaShard(g, bounds, comm.rank)
-    labs, kmax, rounds = sharded_coreness([shard], comm, g.n, approx)
+    if peer:
+        link_ipc(shard, comm)
+    labs, kmax, rounds = sharded_coreness([shard], comm, g.n, approx, peer)
     return _decomposition(np.concatenate(comm.allgather(labs[0])), kmax, rounds, approx)

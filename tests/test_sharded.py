@@ -167,3 +167,140 @@ def test_cuda_shards_from_own_rows(orc, dg):
     del g  # shards own their rows
     labs, k, rr = sharded_coreness(shards, LocalComm(4), hg.n)
     np.testing.assert_array_equal(np.concatenate(labs), lab)
+
+
+# ------------------------------------------------------------------ peer mode (fused rounds)
+@pytest.mark.parametrize("P", [1, 2, 3, 5])
+def test_peer_protocol_numpy_local(orc, P):
+    from shard_numpy import NumpyPeerShard
+    from paper_2311_04333_b200.sharded import link_local
+    for name, g in _graphs(orc).items():
+        for approx in APPROX:
+            b = partition(g.offs, P)
+            shards = [NumpyPeerShard(g.offs, g.adj, b, r) for r in range(P)]
+            link_local(shards)
+            labs, kmax, rounds = sharded_coreness(shards, LocalComm(P, "cpu"), g.n, approx,
+                                                  peer=True)
+            _check(orc, g, labs, kmax, rounds, approx)
+
+
+def _gloo_peer_worker(rank, world, port, outdir):
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "oracle"))
+    import torch.distributed as dist
+    from oracle import Oracle
+    from shard_numpy import NumpyPeerShard
+    from paper_2311_04333_b200.sharded import link_ipc
+
+    class Serial(NumpyPeerShard):  # one rank at a time inside a round (any order is valid)
+        def expand_peer(self, bound, label):
+            made = 0
+            for turn in range(world):
+                if turn == rank:
+                    made = super().expand_peer(bound, label)
+                dist.barrier()
+            return made
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        res = {}
+        for name, g in _graphs(orc).items():
+            for ai, approx in enumerate(APPROX):
+                b = partition(g.offs, world)
+                comm = TorchComm("cpu")
+                shard = Serial(g.offs, g.adj, b, rank, shm=True)
+                link_ipc(shard, comm)
+                labs, kmax, rounds = sharded_coreness([shard], comm, g.n, approx, peer=True)
+                full = np.concatenate(comm.allgather(labs[0]))
+                dist.barrier()  # nobody maps this block any more
+                shard.close()
+                res[f"{name}/{ai}"] = (full, kmax, rounds)
+        if rank == 0:
+            np.save(os.path.join(outdir, "res.npy"), res, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_gloo_world2(orc):
+    """world_size-2 run of the fused protocol: the shard state blocks are
+    shared memory mapped by the other process (the CPU stand-in for CUDA IPC
+    over NVLink), one all-reduce per round."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_gloo_peer_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = np.load(os.path.join(d, "res.npy"), allow_pickle=True).item()
+    gs = _graphs(orc)
+    for name, g in gs.items():
+        for ai, approx in enumerate(APPROX):
+            full, kmax, rounds = res[f"{name}/{ai}"]
+            _check(orc, g, [full], kmax, rounds, approx)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 4, 7])
+def test_cuda_shards_peer_local(orc, dg, P):
+    """Peer-mode kernels: P shards on one GPU decrement each other's state
+    blocks directly (the same kernel maps NVLink peer memory across GPUs)."""
+    from paper_2311_04333_b200.sharded import coreness_local_shards
+    for name, hg in _graphs(orc).items():
+        g = dg.Graph.from_csr(hg.offs, hg.adj, hg.orig)
+        for approx in APPROX:
+            dec = coreness_local_shards(g, P, approx, peer=True)
+            _check(orc, hg, [dec.labels], dec.kmax, dec.peel_rounds, approx)
+
+
+def _ipc_worker(rank, world, port, outdir):
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "oracle"))
+    import torch.distributed as dist
+    from oracle import Oracle
+    import paper_2311_04333_b200 as dg
+    from paper_2311_04333_b200.sharded import CudaShard, link_ipc
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        res = {}
+        gs = _graphs(orc)
+        for name in ("rmat10", "planted", "tri_pendant"):
+            hg = gs[name]
+            g = dg.Graph.from_csr(hg.offs, hg.adj, hg.orig)
+            b = partition(hg.offs, world)
+            comm = TorchComm("cpu")
+            shard = CudaShard(g, b, rank)
+            link_ipc(shard, comm)  # the other process's state block, by CUDA IPC
+            for ai, approx in enumerate(APPROX):
+                if ai:  # fresh state per run
+                    dist.barrier()
+                    del shard
+                    shard = CudaShard(g, b, rank)
+                    link_ipc(shard, comm)
+                labs, kmax, rounds = sharded_coreness([shard], comm, hg.n, approx, peer=True)
+                res[f"{name}/{ai}"] = (np.concatenate(comm.allgather(labs[0])), kmax, rounds)
+            dist.barrier()  # nobody maps the blocks any more
+            del shard
+        if rank == 0:
+            np.save(os.path.join(outdir, "res.npy"), res, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_cuda_peer_ipc_two_processes(orc):
+    """The IPC path of peer mode: two processes (gloo for the host
+    collectives) map each other's shard state with cudaIpcOpenMemHandle and
+    run the fused rounds.  Both processes share the one GPU here; no kernel
+    waits on the other process (rounds are separated by the host all-reduce)."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_ipc_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = np.load(os.path.join(d, "res.npy"), allow_pickle=True).item()
+    gs = _graphs(orc)
+    for name in ("rmat10", "planted", "tri_pendant"):
+        for ai, approx in enumerate(APPROX):
+            full, kmax, rounds = res[f"{name}/{ai}"]
+            _check(orc, gs[name], [full], kmax, rounds, approx)

@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 import paper_2311_04333_b200 as dg
-from paper_2311_04333_b200.sharded import CudaShard, LocalComm, sharded_coreness
+from paper_2311_04333_b200.sharded import CudaShard, LocalComm, link_local, sharded_coreness
 from paper_2311_04333_b200.sharded_build import build_shards, gather_rows, shard_get_core
 
 
@@ -48,6 +48,12 @@ def main():
             c = t()
             labs, kmax, rounds = sharded_coreness(shards, comm, n)
             d = t()
+            shards = [CudaShard.from_rows(n, bounds, r, o, x) for r, (o, x, _) in enumerate(rows)]
+            link_local(shards)
+            c2 = t()
+            labs2, kmax2, rounds2 = sharded_coreness(shards, comm, n, peer=True)
+            d2 = t()
+            assert np.array_equal(np.concatenate(labs2), np.concatenate(labs)) and rounds2 == rounds
             thresh = (kmax + 1) // 2
             _, _, crow, clab = shard_get_core(comm, bounds, rows, labs, thresh)
             e = t()
@@ -56,7 +62,8 @@ def main():
             del shards
         assert np.array_equal(np.concatenate(labs), dec.labels) and kmax == dec.kmax
         out[f"P{P}"] = {"build_ms": (b - a) * 1e3, "shard_create_ms": (c - b) * 1e3,
-                        "coreness_ms": (d - c) * 1e3, "rounds": rounds,
+                        "coreness_ms": (d - c) * 1e3, "coreness_peer_ms": (d2 - c2) * 1e3,
+                        "rounds": rounds,
                         "get_core_ms": (e - d) * 1e3, "gather_ms": (f - e) * 1e3,
                         "core_n": len(orig), "core_arcs": int(offs[-1])}
     print(json.dumps(out))
