@@ -32,7 +32,7 @@ from typing import List, Sequence
 import numpy as np
 
 __all__ = ["partition", "TorchComm", "LocalComm", "CudaShard", "sharded_coreness",
-           "coreness_local_shards", "coreness_distributed", "link_local", "link_ipc"]
+           "coreness_local_shards", "coreness_distributed", "link", "link_local", "link_ipc"]
 
 
 def partition(offs: np.ndarray, P: int) -> np.ndarray:
@@ -298,6 +298,15 @@ def link_ipc(shard, comm):
     for r, h in enumerate(handles):
         if r != comm.rank:
             shard.peer_open(r, h)
+
+
+def link(shards: List, comm):
+    """Peer mode wiring for whichever communicator holds the shards."""
+    if isinstance(comm, LocalComm):
+        link_local(shards)
+    else:
+        for sh in shards:
+            link_ipc(sh, comm)
 
 
 def sharded_coreness(shards: List, comm, n_global: int, approx=None, peer: bool = False):

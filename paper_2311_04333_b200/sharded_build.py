@@ -211,20 +211,22 @@ def gather_rows(comm, rows, labels):
     return offs, adj, orig, lab
 
 
-def prune_distributed(pairs, comm, make_shard, cfg):
+def prune_distributed(pairs, comm, make_shard, cfg, peer: bool = False):
     """framework.cpp:58-79 on the shards: distributed build, sharded coreness
     (exact, or approximate for approx/hybrid), first threshold, per-shard
     get_core, one gather.  Returns (core offs, adj, orig, core labels, kmax,
     peel_rounds) on every rank -- the input of run_pruned.
     make_shard(n, bounds, rank, offs, adj) -> a shard engine."""
     from . import Density, ceil_scaled
-    from .sharded import sharded_coreness
+    from .sharded import link, sharded_coreness
     if cfg.pruning == "none":
         raise ValueError("the sharded pipeline prunes; use run() for pruning='none'")
     approx = None if cfg.pruning == "exact" else (cfg.c_num, cfg.c_den)
     n, bounds, rows = build_shards(pairs, comm)
     shards = [make_shard(n, bounds, r, o, a) for r, (o, a, _) in zip(comm.shards(), rows)]
-    labs, kmax, rounds = sharded_coreness(shards, comm, n, approx)
+    if peer:
+        link(shards, comm)
+    labs, kmax, rounds = sharded_coreness(shards, comm, n, approx, peer)
     del shards
     lower = Density(kmax, 2)
     thresh = ceil_scaled(lower, 1, 1) if approx is None else ceil_scaled(lower, cfg.c_den,
@@ -246,6 +248,6 @@ def run_distributed(u, v, cfg=None):
     cfg = cfg or RunConfig()
     comm = TorchComm(torch.device("cuda", torch.cuda.current_device()))
     offs, adj, orig, lab, kmax, rounds = prune_distributed([(u, v)], comm, CudaShard.from_rows,
-                                                           cfg)
+                                                           cfg, peer=True)
     return run_pruned(Graph.from_device_csr(offs, adj, orig), lab.cpu().numpy(), kmax, rounds,
                       cfg)

@@ -273,7 +273,7 @@ def test_run_pruned_matches_run(orc, dg, P):
                 cfg = dg.RunConfig(algorithm=algorithm, pruning=pruning, iterations=6)
                 pairs = [(a.cuda(), b.cuda()) for a, b in _split(u, v, P)]
                 offs, adj, orig, lab, kmax, rounds = prune_distributed(
-                    pairs, LocalComm(P), CudaShard.from_rows, cfg)
+                    pairs, LocalComm(P), CudaShard.from_rows, cfg, peer=(P > 1))
                 got = dg.run_pruned(dg.Graph.from_device_csr(offs, adj, orig),
                                     lab.cpu().numpy(), kmax, rounds, cfg)
                 want = dg.run(g, cfg)
