@@ -179,6 +179,7 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
   if (cfg->algorithm < 0 || cfg->algorithm > 1 || cfg->pruning < 0 || cfg->pruning > 3)
     throw DgError(DG_E_PARAM, "unknown algorithm or pruning mode");
   *res = dg_run_result{};
+  Nvtx rrun("dg.run");
   const double t0 = now_ms();
   Events span;
   DG_CUDA(cudaEventRecord(span.e[0], stream()));
@@ -232,7 +233,11 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
     const double c0 = now_ms();
     const bool approx = cfg->pruning != 1;
     DevBuf<uint32_t> lab(g->n), map(g->n);
-    CoreOut co = coreness(*g, approx, cfg->c_num, cfg->c_den, lab.get());
+    CoreOut co = [&] {
+      Nvtx r("dg.coreness");
+      return coreness(*g, approx, cfg->c_num, cfg->c_den, lab.get());
+    }();
+    Nvtx rg("dg.get_core");
     res->coreness_kernel_ms = co.kernel_ms;
     res->peel_rounds = co.rounds;
     le = co.kmax;
@@ -280,6 +285,7 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
     const uint64_t n = cur->n;
     DG_CUDA(cudaEventRecord(ev.e[0], stream()));
     if (cfg->algorithm == 0) {
+      Nvtx r("dg.order");
       peel_order(*cur, loads.get(), kr, false, perm.get(), raw.get(), dbat.get());
     } else {
       sort_order(n, loads.get(), perm.get());
@@ -288,6 +294,7 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
     }
     DG_CUDA(cudaEventRecord(ev.e[1], stream()));
     const uint64_t allowed = cfg->algorithm == 0 ? delta_cur : 0;
+    Nvtx ru("dg.update");
     alg3(*cur, perm.get(), cfg->algorithm == 0 ? nullptr : charges.get(),
          cfg->algorithm == 0 ? raw.get() : nullptr, kr.min_load, loads.get(), cfg->slack_samples,
          allowed,
@@ -332,6 +339,7 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
       if (nt > thresh) {
         const double r0 = now_ms();
         DevBuf<uint32_t> map(n);
+        Nvtx rr("dg.reprune");
         GraphPtr next = induced(*cur, nullptr, labels.get(),
                                 uint32_t(std::min<uint64_t>(nt, 0xffffffffULL)), map.get());
         if (next->n == 0) throw DgError(DG_E_INVARIANT, "re-pruning removed every vertex");
@@ -361,6 +369,7 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
   res->iterations = T;
 
   // witness ascending (framework.cpp:156), recount on the input graph (:159-175)
+  Nvtx rw("dg.witness");
   sort_u64(wit.get(), nwit);
   {
     DevBuf<uint8_t> in(g->n);

@@ -3,6 +3,8 @@
 
 #include <memory>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 // Device-resident CSR (reference Graph, graph.hpp:24-45): offs u64[n+1],
@@ -15,6 +17,15 @@ struct dg_graph {
 };
 
 namespace dgb {
+
+// NVTX range for the phases of the path (header-only NVTX v3: a no-op unless
+// a profiler is attached; ncu --nvtx --nvtx-include "dg.order/" etc.)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 using GraphPtr = std::unique_ptr<dg_graph>;
 

@@ -3,6 +3,7 @@
 //   cache_check roundtrip <in.dgrc> <out.dgrc>   read, print "n m source_hash", write back
 //   cache_check hash <file>                      print hash_file(file)
 //   cache_check is <file>                        print is_cache_file(file)
+//   cache_check fnv <string>                     print fnv1a64 of its bytes
 // Exit codes follow the reference CLI mapping (densest.cpp:305-329):
 // Io 3, Invariant 4, CacheHash 6.
 #include <cstdio>
@@ -25,6 +26,11 @@ int main(int argc, char** argv) {
     }
     if (mode == "hash") {
       std::printf("%llu\n", (unsigned long long)hash_file(argv[2]));
+      return 0;
+    }
+    if (mode == "fnv") {  // fnv1a64 of the argument's bytes
+      const std::string x = argv[2];
+      std::printf("%llu\n", (unsigned long long)fnv1a64(x.data(), x.size()));
       return 0;
     }
     if (mode == "is") {

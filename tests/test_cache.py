@@ -49,6 +49,13 @@ def test_cache_roundtrip_is_byte_identical(exe, tmp_path, name):
     assert _run(exe, "is", os.path.join(GOLD, c["text"])).stdout.strip() == "0"
 
 
+def test_fnv1a64_vectors(exe):
+    """The published FNV-1a 64-bit test vectors (offset basis 0xcbf29ce484222325,
+    prime 0x100000001b3), the hash behind hash_file and the cache payload check."""
+    for text, want in (("a", 0xaf63dc4c8601ec8c), ("foobar", 0x85944171f73967e8)):
+        assert int(_run(exe, "fnv", text).stdout) == want, text
+
+
 def test_cache_errors(exe, tmp_path):
     gold = open(os.path.join(GOLD, "cache_lcg.dgrc"), "rb").read()
     bad = tmp_path / "bad.dgrc"
