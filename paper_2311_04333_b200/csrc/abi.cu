@@ -288,9 +288,10 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
       Nvtx r("dg.order");
       peel_order(*cur, loads.get(), kr, false, perm.get(), raw.get(), dbat.get());
     } else {
-      sort_order(n, loads.get(), perm.get());
+      Nvtx r("dg.order");
+      sort_order_range(n, loads.get(), kr, perm.get());
       if (charges.n != n) charges.alloc(n);
-      charges_from_perm(*cur, perm.get(), charges.get());
+      charges_trusted(*cur, perm.get(), charges.get());
     }
     DG_CUDA(cudaEventRecord(ev.e[1], stream()));
     const uint64_t allowed = cfg->algorithm == 0 ? delta_cur : 0;

@@ -82,6 +82,10 @@ void sort_order(uint64_t n, const uint64_t* d_loads, uint32_t* d_perm);
 // A[i] from an arbitrary permutation (refine.cpp:186-199); throws InvariantError
 // on a non-permutation.
 void charges_from_perm(const dg_graph& g, const uint32_t* d_perm, uint32_t* d_charges);
+// run()-internal forms: the stable (load, id) sort on just the bits the load
+// range needs, and charges from a permutation known to be valid
+void sort_order_range(uint64_t n, const uint64_t* d_loads, const KeyRange& kr, uint32_t* d_perm);
+void charges_trusted(const dg_graph& g, const uint32_t* d_perm, uint32_t* d_charges);
 
 struct Alg3Out {  // device-written scalars of one update
   uint64_t rho_edges, rho_verts, best_prefix, width;

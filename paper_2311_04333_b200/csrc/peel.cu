@@ -217,16 +217,32 @@ __global__ void k_pos_from_perm(const uint32_t* perm, uint64_t n, uint64_t* pos,
   }
 }
 
-__global__ void k_charges(const uint64_t* offs, const uint32_t* adj, uint64_t n,
-                          const uint64_t* pos, uint32_t* A) {
+// A[pos(v)] = #neighbours positioned after v (refine.cpp:195-199: every edge
+// charged to its earlier endpoint): a warp per row counts them and writes its
+// own position -- no atomics, no zero fill
+template <class P>
+__global__ void k_charges_rows(const uint64_t* offs, const uint32_t* adj, uint64_t n,
+                               const P* pos, uint32_t* A) {
   const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t v = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; v < n; v += warps) {
-    const uint64_t pv = pos[v];
-    for (uint64_t p = offs[v] + lane_id(); p < offs[v + 1]; p += 32) {
-      const uint32_t u = adj[p];
-      if (u > v) atomicAdd(&A[min(pv, pos[u])], 1u);
-    }
+    const P pv = pos[v];
+    uint32_t c = 0;
+    for (uint64_t p = offs[v] + lane_id(); p < offs[v + 1]; p += 32) c += pos[adj[p]] > pv;
+    c = __reduce_add_sync(~0u, c);
+    if (lane_id() == 0) A[pv] = c;
   }
+}
+
+__global__ void k_pos32(const uint32_t* perm, uint64_t n, uint32_t* pos) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    pos[perm[i]] = uint32_t(i);
+}
+
+__global__ void k_sort_keys32(const uint64_t* loads, uint64_t n, uint64_t base, uint32_t* keys) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    keys[i] = uint32_t(loads[i] - base);
 }
 
 __global__ void k_iota(uint32_t* p, uint64_t n) {
@@ -509,10 +525,46 @@ void charges_from_perm(const dg_graph& g, const uint32_t* d_perm, uint32_t* d_ch
   k_pos_from_perm<<<grid_for(n, 256), 256, 0, stream()>>>(d_perm, n, pos.get(), err.get());
   DG_CHECK_LAUNCH();
   if (read_scalar(err.get())) throw DgError(DG_E_INVARIANT, "ordering is not a permutation");
-  DG_CUDA(cudaMemsetAsync(d_charges, 0, n * sizeof(uint32_t), stream()));
-  k_charges<<<grid_for(n * 32, 256), 256, 0, stream()>>>(g.offs.get(), g.adj.get(), n, pos.get(),
-                                                         d_charges);
+  k_charges_rows<uint64_t><<<grid_for(n * 32, 256), 256, 0, stream()>>>(g.offs.get(), g.adj.get(),
+                                                                         n, pos.get(), d_charges);
   DG_CHECK_LAUNCH();
+}
+
+void charges_trusted(const dg_graph& g, const uint32_t* d_perm, uint32_t* d_charges) {
+  const uint64_t n = g.n;
+  if (!n) return;
+  DevBuf<uint32_t> pos(n);
+  k_pos32<<<grid_for(n, 256), 256, 0, stream()>>>(d_perm, n, pos.get());
+  DG_CHECK_LAUNCH();
+  k_charges_rows<uint32_t><<<grid_for(n * 32, 256), 256, 0, stream()>>>(g.offs.get(), g.adj.get(),
+                                                                         n, pos.get(), d_charges);
+  DG_CHECK_LAUNCH();
+}
+
+void sort_order_range(uint64_t n, const uint64_t* d_loads, const KeyRange& kr, uint32_t* d_perm) {
+  if (!n) return;
+  uint32_t bits = 0;
+  while (bits < 64 && (kr.max_key >> bits)) ++bits;  // loads - base <= max_key
+  if (bits > 32) {
+    sort_order(n, d_loads, d_perm);
+    return;
+  }
+  if (bits == 0) {
+    k_iota<<<grid_for(n, 256), 256, 0, stream()>>>(d_perm, n);
+    DG_CHECK_LAUNCH();
+    return;
+  }
+  DevBuf<uint32_t> ids(n), k32(n), ks(n);
+  k_iota<<<grid_for(n, 256), 256, 0, stream()>>>(ids.get(), n);
+  DG_CHECK_LAUNCH();
+  k_sort_keys32<<<grid_for(n, 256), 256, 0, stream()>>>(d_loads, n, kr.min_load, k32.get());
+  DG_CHECK_LAUNCH();
+  size_t tmp = 0;
+  DG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k32.get(), ks.get(), ids.get(), d_perm, n,
+                                          0, int(bits), stream()));
+  DevBuf<char> t(tmp);
+  DG_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, k32.get(), ks.get(), ids.get(), d_perm, n,
+                                          0, int(bits), stream()));
 }
 
 void alg3(const dg_graph& g, const uint32_t* d_perm, const uint32_t* d_charges,
