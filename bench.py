@@ -318,6 +318,16 @@ def run_ours(args, cfg, rank, world, local):
         "clocks": clk,
     }
 
+    # ---- the GreedySorting++ variant on the same graph,
+    # outside the timed region: informational, same edges/s definition
+    sres = dg.run(g, dg.RunConfig(algorithm="sort", iterations=cfg["T"], epsilon=cfg["eps"]))
+    s_edges = sum(it.m for it in sres.trace.iters)
+    s_ms = sum(it.ms for it in sres.trace.iters)
+    line["sort_variant"] = {"value": s_edges / (s_ms / 1e3), "unit": "edges/s",
+                            "ms_per_iter": s_ms / max(1, len(sres.trace.iters)),
+                            "best": [sres.best.edges, sres.best.verts],
+                            "note": "algorithm=sort (refine.cpp:158-178), not the headline"}
+
     # ---- e2e through the C ABI from pinned host buffers
     offs, adj, orig = g.download()
     p_offs, _t1 = pinned_copy(offs)
