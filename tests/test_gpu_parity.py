@@ -580,3 +580,26 @@ def test_coreness_level_advance_paths(dg, orc):
             a = dg.approx_coreness(g, cn, cd)
             al, ak, ar = orc.coreness(h, True, cn, cd)
             assert np.array_equal(a.labels, al) and (a.kmax, a.peel_rounds) == (ak, ar), (cn, cd)
+
+
+@pytest.mark.gpu
+def test_peel_large_cores_cluster_and_global_keys(dg, orc):
+    """Cores beyond one SM: a ~200K-vertex core (16-CTA cluster kernel, keys in
+    distributed shared memory) and a ~600K-vertex core (single-CTA kernel with
+    its keys in global memory) give the oracle's peel order and loads, batch
+    and (on the smaller one) one-at-a-time (refine.cpp:20-156, 180-220)."""
+    for n, m in ((200000, 1600000), (600000, 4800000)):
+        u, v = orc.gen_er_planted(n, m, 40, 3)
+        h = orc.build(u, v)
+        lab, k, _ = orc.coreness(h)
+        core, _ = orc.get_core(h, lab, (k + 1) // 2)
+        g = dg.Graph.from_csr(core.offs, core.adj, core.orig)
+        rng = np.random.default_rng(n)
+        ld = rng.integers(0, 64, core.n).astype(np.uint64)
+        lh = ld.copy()
+        for one in ((False, True) if n < 400000 else (False,)):
+            p = dg.load_peel_order(g, ld, one_at_a_time=one).perm
+            assert np.array_equal(p, orc.peel_order(core, lh, one)), (n, one)
+        dg.density_and_load_update(g, p, ld)
+        _, lh, _, _ = orc.density_update(core, p, lh)
+        assert np.array_equal(ld, lh)
