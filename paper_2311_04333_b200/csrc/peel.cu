@@ -376,6 +376,7 @@ bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, b
   const uint64_t n = g.n;
   uint32_t sh = 10;  // NC = 2^sh >= PT ids per CTA
   while ((uint64_t(CS) << sh) < n) ++sh;
+  if (sh > 15) return false;  // <= 32 keys per thread (the S1 match mask)
   const bool offs32 = 2 * g.m < 0xffffffffULL;
   bool offs_smem = offs32 && peelc::smem_bytes(sh, true) <= kSmemCap;
   if (!offs_smem && peelc::smem_bytes(sh, false) > kSmemCap) return false;
@@ -409,6 +410,8 @@ bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, b
     cudaGetLastError();
     return false;
   }
+  // raw charges are accumulated with atomics (see peel_cluster.cuh)
+  DG_CUDA(cudaMemsetAsync(d_raw, 0, n * sizeof(uint64_t), stream()));
   peelc::Args a{g.offs.get(), g.adj.get(), uint32_t(n), d_loads, base, one ? 1 : 0,
                 sh, (1u << sh) / peelc::PT, offs_smem ? 1 : 0, d_perm, d_raw, d_batches,
                 peel_prof_buffer()};

@@ -1,25 +1,42 @@
 // peel_cluster.cuh -- Greedy++ batch peel over a thread-block CLUSTER, for
 // cores whose keys do not fit one SM's shared memory (e.g. RMAT-26's
-// 83,682-vertex ceil(kmax/2)-core, RMAT-22's 35,367-vertex one).
+// 83,682-vertex ceil(kmax/2)-core, RMAT-28's 122K one).
 //
 // Same semantics and key ranges as peel_kernel.cuh (refine.cpp:20-156, fused
 // Alg. 3 charges).  The vertex range is split into CS contiguous blocks of NC
 // = 2^sh ids; CTA r of the cluster owns keys [r*NC, (r+1)*NC) (and their u32
-// row offsets) in its shared memory.  Per batch:
-//   S1  every CTA scans its own keys (128-bit loads), CTA-level (min, count)
-//       via redux.sync + one CTA barrier, published in its shared memory
-//   --- cluster barrier A
-//   S2  every warp reads the CS CTA summaries through DSMEM (one remote load
-//       per lane) -> global min, batch size, its CTA's offset; owners write
-//       the batch in ascending id (CTA order = id order) into perm, the raw
-//       charge key_at_removal into raw[pos], and broadcast (v, row offset,
-//       degree) of the first 32 members into every CTA's staging slots
-//   --- cluster barrier B
-//   S3  the cluster's warps share the members' rows (16-byte quads); every
-//       neighbour's key is decremented with a DSMEM reduction on its owner
-//       CTA (atom.shared::cluster when same-batch neighbours must be told
-//       apart, whose decrements then go to raw[pos] in global memory)
-//   --- cluster barrier C
+// row offsets) in its shared memory.
+//
+// Owner-applied decrements.  Every CTA streams the removed members' rows
+// (16-byte quads from L2) and applies only the decrements whose target lies
+// in its own block, with shared-memory atomics on its own keys: no atomic
+// ever crosses the cluster, and the row is read CS times from L2 (a few KB
+// per member, far below L2 bandwidth).
+//
+// Per batch (no cluster-wide barrier on the common path):
+//   S1  every CTA scans its own keys: (min, count, first id at the min, its
+//       degree and row start) = its 32-byte summary, which warp 0 PUSHES
+//       into every CTA's shared memory with st.async (slot [parity][rank])
+//       completing bytes on the receiver's mbarrier; each CTA waits on its
+//       own mbarrier for the CS summaries (no cluster.sync: that costs
+//       ~380 cycles plus an L1 invalidate, and reading the summaries
+//       remotely queues every warp's requests on one SM's shared memory)
+//   S2  every warp decodes the local summaries -> global min, owner CTAs,
+//       batch size.  Simple batch (each owner CTA holds exactly one
+//       member, or one-at-a-time): the summaries name the batch in
+//       ascending id (CTA order = id order), so every CTA starts removing at
+//       once.  Otherwise owners write the batch and push (v, degree, row
+//       start) of each member into every CTA's staging slots (again
+//       st.async on a second mbarrier pair).
+//   S3  removal, owner-applied (above); batches beyond SB members decrement
+//       through DSMEM instead (remote atomics between cluster barriers)
+//   --- CTA barrier (the next S1 reads only this CTA's keys)
+// Slots are double-buffered by batch parity: a CTA pushes batch b+2's
+// summary only after receiving every CTA's b+1 summary, which each CTA
+// sends after it has decoded batch b.
+// Raw charges (key_at_removal - #same-batch neighbours with a smaller id)
+// are accumulated with atomics into a zeroed raw[]: the owner adds the key,
+// every CTA subtracts the same-batch arcs it sees, in any order.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -46,23 +63,122 @@ struct Args {
   uint32_t chunk;  // keys per thread = NC / PT (multiple of 4 when >= 4)
   int offs_smem;   // row offsets staged in shared memory (u32)
   uint32_t* perm;
-  uint64_t* raw;
+  uint64_t* raw;   // zeroed by the launcher
   unsigned long long* batches;
-  unsigned long long* prof;  // [8] rank-0 thread-0 cycles: S1, S2, S3, batches
+  unsigned long long* prof;  // [8] rank-0 thread-0 cycles: S1, S2, S3, batches, simple
+};
+
+// CTA summary: min key, #keys at the min, first id at the min, its degree,
+// its row start (u64) -- two 16-byte st.async
+struct __align__(16) Summary {
+  uint32_t cmin, ccnt, cfirst, cdeg;
+  uint32_t r0lo, r0hi, pad0, pad1;
+};
+
+// staged member of a general batch: id, degree, row start
+struct __align__(16) Member {
+  uint32_t v, deg, r0lo, r0hi;
 };
 
 struct Fixed {
-  uint32_t bv[SB];
-  uint64_t boff[SB];
-  uint32_t bdeg[SB];
+  unsigned long long mbA[2], mbB[2];  // summaries / staged members, by parity
+  Summary sum[2][16];                 // [parity][CTA rank]
+  Member stage[2][SB];                // [parity][member]
   uint32_t wmin[NW];
   uint32_t wcnt[NW];
-  uint32_t cmin, ccnt;  // this CTA's summary (read remotely)
+  uint32_t wfirst[NW];
+  // warp -> member map over this CTA's warps for batches of b <= SB members:
+  // wmap[b-1][w] = j | rank << 8 | nwj << 16 (j = w % b, rank = w / b,
+  // nwj = #warps serving member j)
   uint32_t wmap[SB][NW];
 };
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+// shared::cluster address of `local` in CTA `r`
+__device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t r) {
+  uint32_t o;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(local), "r"(r));
+  return o;
+}
+__device__ __forceinline__ void st_async(uint32_t raddr, const uint4& v, uint32_t rbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::
+          "r"(raddr),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// row [oj, oj + dj) of member vj, quads [rk*32 + lane, ...) step nwj*32:
+// decrement the targets in this CTA's block [gbase, gbase + NC)
+template <bool ONE>
+__device__ __forceinline__ void remove_local(const uint4* adj4, uint32_t keys_s, uint64_t oj,
+                                             uint32_t dj, uint32_t vj, uint32_t rk, uint32_t nwj,
+                                             uint32_t lane, uint32_t gbase, uint32_t NC,
+                                             unsigned long long* rawj) {
+  const uint64_t ej = oj + dj, q1 = (ej + 3) >> 2, stride = uint64_t(nwj) * 32;
+  for (uint64_t b0 = (oj >> 2) + uint64_t(rk) * 32 + lane; b0 < q1; b0 += stride * UQ) {
+    uint4 x[UQ];
+#pragma unroll
+    for (int k = 0; k < UQ; ++k)
+      if (b0 + k * stride < q1) x[k] = __ldg(adj4 + b0 + k * stride);
+#pragma unroll
+    for (int k = 0; k < UQ; ++k) {
+      const uint64_t q = b0 + k * stride;
+      if (q >= q1) break;
+      const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+      bool ok[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t p = (q << 2) + e;
+        ok[e] = p >= oj && p < ej && us[e] - gbase < NC;
+      }
+      if (ONE) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (ok[e])
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(keys_s + ((us[e] - gbase) << 2)),
+                         "r"(0xffffffffu)
+                         : "memory");
+      } else {
+        uint32_t old[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {  // all atomics in flight before any test
+          old[e] = 0;
+          if (ok[e])
+            asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                         : "=r"(old[e])
+                         : "r"(keys_s + ((us[e] - gbase) << 2)), "r"(0xffffffffu)
+                         : "memory");
+        }
+        unsigned long long c = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c += (ok[e] && Range<uint32_t>::in_batch(old[e]) && us[e] < vj);
+        if (c) atomicAdd(rawj, 0ULL - c);
+      }
+    }
+  }
+}
+
 template <int CS>
 __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
+  static_assert(CS <= 16, "summary slots");
   using R = Range<uint32_t>;
   cg::cluster_group cl = cg::this_cluster();
   const uint32_t rank = cl.block_rank();
@@ -77,6 +193,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   const uint32_t n = a.n, c = a.chunk, lo = tid * c, hi = lo + c;
   const uint32_t gbase = rank << a.sh;  // first global id owned by this CTA
   const bool vec = (c & 3u) == 0;
+  const uint32_t keys_s = smem_u32(keys);
 
   for (uint32_t i = lo; i < hi; ++i) {
     const uint32_t g = gbase + i;
@@ -91,22 +208,36 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   }
   if (a.offs_smem && tid == 0) soffs[NC] = uint32_t(a.offs[min(n, gbase + NC)]);
   for (uint32_t e = tid; e < SB * NW; e += PT) {
-    const uint32_t b = e / NW + 1, ww = e % NW, gw = rank * NW + ww;
-    const uint32_t jj = gw % b;
-    // (member, rank among its warps, #warps serving it) over the cluster's warps
-    // 8-bit member, 12-bit rank, 12-bit warp count (cluster has up to 512 warps)
-    s.wmap[b - 1][ww] = jj | ((gw / b) << 8) | (((CS * NW - 1 - jj) / b + 1) << 20);
+    const uint32_t b = e / NW + 1, ww = e % NW;
+    const uint32_t jj = ww % b;
+    s.wmap[b - 1][ww] = jj | ((ww / b) << 8) | (((NW - 1 - jj) / b + 1) << 16);
   }
-  cl.sync();
+  if (tid == 0) {
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(smem_u32(&s.mbA[k]));
+      mbar_init(smem_u32(&s.mbB[k]));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cl.sync();  // every CTA's mbarriers exist before the first push
 
-  uint32_t removed = 0, pos = 0;
-  bool marked = false;
-  unsigned long long nbat = 0;
+  uint32_t removed = 0, pos = 0, useB = 0;  // useB bit k: phase parity of mbB[k]
+  bool marked = false;  // my chunk holds BATCH marks of the previous batch
+  unsigned long long nbat = 0, nsimple = 0;
   const bool P = rank == 0 && tid == 0;
   long long c1 = 0, c2 = 0, c3 = 0, tm = clock64();
   while (removed < n) {
+    const uint32_t par = uint32_t(nbat & 1);
+    const uint32_t mbA = smem_u32(&s.mbA[par]), mbB = smem_u32(&s.mbB[par]);
+    // ---- retire my BATCH marks (no decrement of this CTA's keys runs
+    // between the last CTA barrier and the next removal)
+    if (marked) {
+      for (uint32_t i = lo; i < hi; ++i)
+        if (R::in_batch(keys[i])) keys[i] = R::DEAD;
+      marked = false;
+    }
     // ---- S1: CTA summary
-    uint32_t lmin = R::DEAD, lcnt = 0;
+    uint32_t lmin = R::DEAD, bits = 0;  // bits: my keys at lmin (chunk <= 32)
     if (vec) {
       const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
       for (uint32_t q = 0; q < (c >> 2); ++q) {
@@ -115,142 +246,185 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       }
       for (uint32_t q = 0; q < (c >> 2); ++q) {
         const uint4 v = kv[q];
-        lcnt += uint32_t(v.x == lmin) + uint32_t(v.y == lmin) + uint32_t(v.z == lmin) +
-                uint32_t(v.w == lmin);
+        bits |= ((v.x == lmin) | ((v.y == lmin) << 1) | ((v.z == lmin) << 2) |
+                 (uint32_t(v.w == lmin) << 3))
+                << (4 * q);
       }
     } else {
       for (uint32_t i = lo; i < hi; ++i) lmin = min(lmin, keys[i]);
-      for (uint32_t i = lo; i < hi; ++i) lcnt += keys[i] == lmin;
+      for (uint32_t i = lo; i < hi; ++i) bits |= uint32_t(keys[i] == lmin) << (i - lo);
     }
+    uint32_t lcnt = __popc(bits);
+    const uint32_t lfirst = lo + __ffs(bits) - 1;
     if (!R::alive(lmin)) lmin = R::DEAD, lcnt = 0;
     const uint32_t wm = __reduce_min_sync(~0u, lmin);
     const uint32_t wc = __reduce_add_sync(~0u, lmin == wm ? lcnt : 0u);
+    const uint32_t fl = __ffs(__ballot_sync(~0u, lmin == wm)) - 1;
+    const uint32_t wf = __shfl_sync(~0u, lfirst, fl);
     if (lane == 0) {
       s.wmin[w] = wm;
       s.wcnt[w] = wc;
+      s.wfirst[w] = wf;
     }
+    if (tid == 0) mbar_expect(mbA, CS * uint32_t(sizeof(Summary)));
     __syncthreads();
-    if (w == 0) {
+    if (w == 0) {  // CTA summary, pushed to every CTA (lane q -> CTA q)
       const uint32_t x = s.wmin[lane];
       const uint32_t cm = __reduce_min_sync(~0u, x);
       const uint32_t ccnt = __reduce_add_sync(~0u, x == cm ? s.wcnt[lane] : 0u);
-      if (lane == 0) {
-        s.cmin = cm;
-        s.ccnt = ccnt;
+      const uint32_t fw = __ffs(__ballot_sync(~0u, x == cm)) - 1;
+      const uint32_t f = s.wfirst[fw];
+      uint64_t r0 = 0, r1 = 0;
+      if (R::alive(cm)) {
+        if (a.offs_smem) {
+          r0 = soffs[f];
+          r1 = soffs[f + 1];
+        } else {
+          r0 = a.offs[gbase + f];
+          r1 = a.offs[gbase + f + 1];
+        }
+      }
+      if (lane < CS) {
+        const uint32_t dst = mapa(smem_u32(&s.sum[par][rank]), lane);
+        const uint32_t bar = mapa(mbA, lane);
+        st_async(dst, make_uint4(cm, ccnt, gbase + f, uint32_t(r1 - r0)), bar);
+        st_async(dst + 16, make_uint4(uint32_t(r0), uint32_t(r0 >> 32), 0u, 0u), bar);
       }
     }
-    cl.sync();  // A
+    mbar_wait(mbA, uint32_t(nbat >> 1) & 1u);
     if (P) {
       const long long t = clock64();
       c1 += t - tm;
       tm = t;
     }
-    // ---- S2: cluster min, batch size, offsets; owners write the batch
-    uint32_t rmin = R::DEAD, rcnt = 0;
+    // ---- S2: every warp decodes the CS summaries (lane q <- CTA q)
+    uint32_t rmin = R::DEAD, rcnt = 0, rfirst = 0, rdeg = 0;
+    uint64_t rr0 = 0;
     if (lane < CS) {
-      const Fixed* rs = cl.map_shared_rank(&s, lane);
-      rmin = rs->cmin;
-      rcnt = rs->ccnt;
+      const uint4* rs = reinterpret_cast<const uint4*>(&s.sum[par][lane]);
+      const uint4 p0 = rs[0], p1 = rs[1];
+      rmin = p0.x;
+      rcnt = p0.y;
+      rfirst = p0.z;
+      rdeg = p0.w;
+      rr0 = uint64_t(p1.x) | (uint64_t(p1.y) << 32);
     }
     const uint32_t gmin = __reduce_min_sync(~0u, rmin);
-    const uint32_t total = __reduce_add_sync(~0u, rmin == gmin ? rcnt : 0u);
+    const bool own = lane < CS && rmin == gmin;
+    const uint32_t ownmask = __ballot_sync(~0u, own);
+    const uint32_t total = __reduce_add_sync(~0u, own ? rcnt : 0u);
     const uint32_t bs = a.one ? 1u : total;
-    if (marked) {
-      for (uint32_t i = lo; i < hi; ++i)
-        if (R::in_batch(keys[i])) keys[i] = R::DEAD;
-      marked = false;
-    }
-    if (s.cmin == gmin && wm == gmin) {  // this warp owns part of the batch
-      const uint32_t cta_off = __reduce_add_sync(~0u, (lane < rank && rmin == gmin) ? rcnt : 0u);
-      const uint32_t xw = s.wmin[lane];
-      const uint32_t woff = __reduce_add_sync(~0u, (lane < w && xw == gmin) ? s.wcnt[lane] : 0u);
-      const bool mine = lmin == gmin && lcnt;
-      const uint32_t mm = __ballot_sync(~0u, mine);
-      uint32_t my = cta_off + woff;
-      if (__popc(mm) > 1) {
-        const uint32_t v = mine ? lcnt : 0u;
-        my += warp_incl_scan(v) - v;
-      }
-      if (mine) {
-        for (uint32_t i = lo; i < hi && my < bs; ++i) {
-          if (keys[i] != gmin) continue;
-          const uint32_t g = gbase + i;
-          a.perm[pos + my] = g;
-          a.raw[pos + my] = gmin;  // same-batch smaller neighbours are subtracted in S3
-          keys[i] = bs == 1 ? R::DEAD : R::BATCH;
-          marked = bs != 1;
-          if (my < SB) {
-            uint64_t r0, r1;
-            if (a.offs_smem) {
-              r0 = soffs[i];
-              r1 = soffs[i + 1];
-            } else {
-              r0 = a.offs[g];
-              r1 = a.offs[g + 1];
-            }
-            for (int q = 0; q < CS; ++q) {  // broadcast into every CTA's staging slot
-              Fixed* rs = cl.map_shared_rank(&s, q);
-              rs->bv[my] = g;
-              rs->boff[my] = r0;
-              rs->bdeg[my] = uint32_t(r1 - r0);
-            }
-          }
-          ++my;
-        }
-      }
-    }
-    cl.sync();  // B
-    if (P) {
-      const long long t = clock64();
-      c2 += t - tm;
-      tm = t;
-    }
-    // ---- S3: the cluster's warps share the members' rows
-    const uint32_t msk = NC - 1;
-    auto dec = [&](uint32_t u, uint32_t vj, uint32_t pj) {
-      uint32_t* rk = cl.map_shared_rank(keys, u >> a.sh) + (u & msk);
-      if (bs == 1) {
-        atomicAdd(rk, 0xffffffffu);
-      } else {
-        const uint32_t old = atomicAdd(rk, 0xffffffffu);
-        if (R::in_batch(old) && u < vj)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&a.raw[pos + pj]), ~0ULL);
-      }
-    };
-    if (bs <= SB) {
+    if (a.one || total == uint32_t(__popc(ownmask))) {
+      // ---- simple batch: owner lane L (CTA L) holds member #(owners below L)
+      ++nsimple;
+      const uint32_t rkl = __popc(ownmask & ((1u << lane) - 1u));
       const uint32_t wm3 = s.wmap[bs - 1][w];
-      const uint32_t j = wm3 & 0xffu, rk = (wm3 >> 8) & 0xfffu, nwj = wm3 >> 20;
-      const uint64_t oj = s.boff[j], ej = oj + s.bdeg[j];
-      const uint32_t vj = s.bv[j];
-      const uint64_t q1 = (ej + 3) >> 2, stride = uint64_t(nwj) * 32;
-      for (uint64_t b0 = (oj >> 2) + uint64_t(rk) * 32; b0 < q1; b0 += stride * UQ) {
-        uint4 x[UQ];
-#pragma unroll
-        for (int k = 0; k < UQ; ++k) {
-          const uint64_t q = b0 + k * stride + lane;
-          if (q < q1) x[k] = __ldg(adj4 + q);
+      const uint32_t j = wm3 & 0xffu, rk = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
+      const uint32_t lj = __ffs(__ballot_sync(~0u, own && rkl == j)) - 1;
+      const uint32_t vj = __shfl_sync(~0u, rfirst, lj), dj = __shfl_sync(~0u, rdeg, lj);
+      const uint64_t oj = __shfl_sync(~0u, rr0, lj);
+      // my CTA's member (if any): every warp marks it before its own
+      // decrements (a later mark by another warp only rewrites a batch key)
+      const uint32_t mrk = __popc(ownmask & ((1u << rank) - 1u));
+      if (((ownmask >> rank) & 1u) && mrk < bs) {
+        const uint32_t mv = __shfl_sync(~0u, rfirst, rank);
+        if (lane == 0) {
+          keys[mv - gbase] = bs == 1 ? R::DEAD : R::BATCH;
+          if (w == 0) {
+            a.perm[pos + mrk] = mv;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.raw[pos + mrk]),
+                      (unsigned long long)gmin);
+          }
         }
-#pragma unroll
-        for (int k = 0; k < UQ; ++k) {
-          const uint64_t q = b0 + k * stride + lane;
-          if (q >= q1) continue;
-          const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint64_t p = (q << 2) + e;
-            if (p >= oj && p < ej) dec(us[e], vj, j);
+        if (bs != 1 && mv - gbase - lo < c) marked = true;
+      }
+      __syncwarp();
+      unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
+      if (bs == 1)
+        remove_local<true>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
+      else
+        remove_local<false>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
+      if (P) {
+        const long long t = clock64();
+        c2 += t - tm;
+        tm = t;
+      }
+      __syncthreads();
+    } else {
+      // ---- general batch (bs >= 2): owners write the batch in ascending id
+      if (tid == 0 && bs <= SB) mbar_expect(mbB, bs * uint32_t(sizeof(Member)));
+      if (((ownmask >> rank) & 1u) && wm == gmin) {  // this warp owns part of the batch
+        const uint32_t cta_off = __reduce_add_sync(~0u, (lane < rank && own) ? rcnt : 0u);
+        const uint32_t xw = s.wmin[lane];
+        const uint32_t woff = __reduce_add_sync(~0u, (lane < w && xw == gmin) ? s.wcnt[lane] : 0u);
+        const bool mine = lmin == gmin && lcnt;
+        const uint32_t mm = __ballot_sync(~0u, mine);
+        uint32_t my = cta_off + woff;
+        if (__popc(mm) > 1) {
+          const uint32_t v = mine ? lcnt : 0u;
+          my += warp_incl_scan(v) - v;
+        }
+        if (mine) {
+          for (uint32_t i = lo; i < hi && my < bs; ++i) {
+            if (keys[i] != gmin) continue;
+            const uint32_t g = gbase + i;
+            a.perm[pos + my] = g;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.raw[pos + my]),
+                      (unsigned long long)gmin);
+            keys[i] = R::BATCH;
+            marked = true;
+            if (my < SB && bs <= SB) {
+              uint64_t r0, r1;
+              if (a.offs_smem) {
+                r0 = soffs[i];
+                r1 = soffs[i + 1];
+              } else {
+                r0 = a.offs[g];
+                r1 = a.offs[g + 1];
+              }
+              const uint4 rec = make_uint4(g, uint32_t(r1 - r0), uint32_t(r0), uint32_t(r0 >> 32));
+              const uint32_t src = smem_u32(&s.stage[par][my]);
+              for (uint32_t q = 0; q < CS; ++q) st_async(mapa(src, q), rec, mapa(mbB, q));
+            }
+            ++my;
           }
         }
       }
-    } else {
-      // large batch: CTA r takes members j = r, r + CS, ...; its warps split a row
-      for (uint32_t j = rank; j < bs; j += CS) {
-        const uint32_t vj = a.perm[pos + j];
-        const uint64_t oj = a.offs[vj], ej = a.offs[vj + 1];
-        for (uint64_t p = oj + tid; p < ej; p += PT) dec(a.adj[p], vj, j);
+      if (bs <= SB) {
+        __syncthreads();  // this CTA's batch marks before its decrements
+        mbar_wait(mbB, (useB >> par) & 1u);
+        useB ^= 1u << par;
+        if (P) {
+          const long long t = clock64();
+          c2 += t - tm;
+          tm = t;
+        }
+        const uint32_t wm3 = s.wmap[bs - 1][w];
+        const uint32_t j = wm3 & 0xffu, rk = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
+        const Member& mj = s.stage[par][j];
+        remove_local<false>(adj4, keys_s, uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32), mj.deg,
+                            mj.v, rk, nwj, lane, gbase, NC,
+                            reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
+        __syncthreads();
+      } else {
+        // large batch: CTA r takes members j = r, r + CS, ...; its warps
+        // split a row and decrement through DSMEM on the owner CTA
+        cl.sync();  // perm and every batch mark written
+        const uint32_t msk = NC - 1;
+        for (uint32_t j = rank; j < bs; j += CS) {
+          const uint32_t vj = a.perm[pos + j];
+          const uint64_t oj = a.offs[vj], ej = a.offs[vj + 1];
+          for (uint64_t p = oj + tid; p < ej; p += PT) {
+            const uint32_t u = a.adj[p];
+            uint32_t* rk = cl.map_shared_rank(keys, u >> a.sh) + (u & msk);
+            const uint32_t old = atomicAdd(rk, 0xffffffffu);
+            if (R::in_batch(old) && u < vj)
+              atomicAdd(reinterpret_cast<unsigned long long*>(&a.raw[pos + j]), ~0ULL);
+          }
+        }
+        cl.sync();
       }
     }
-    cl.sync();  // C
     if (P) {
       const long long t = clock64();
       c3 += t - tm;
@@ -267,10 +441,12 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       a.prof[1] = c2;
       a.prof[2] = c3;
       a.prof[3] = nbat;
-      a.prof[4] = a.prof[5] = a.prof[6] = 0;
+      a.prof[4] = nsimple;
+      a.prof[5] = a.prof[6] = 0;
       a.prof[7] = CS;
     }
   }
+  cl.sync();  // no CTA exits while a push into it could be in flight
 }
 
 inline size_t smem_bytes(uint32_t sh, bool offs_smem) {

@@ -146,6 +146,34 @@ __device__ __forceinline__ void dec_key(K* keys, uint32_t keys_s, uint32_t u, ui
   }
 }
 
+// S3 decrement of a full quad of keys.  Multi-member batches: the four
+// returning atomics are issued back to back and only then tested, so their
+// round trips overlap (testing each before the next atomic serialises them:
+// the branch waits for the returned key).
+template <class K, bool SMEM, bool ONE>
+__device__ __forceinline__ void dec_quad(K* keys, uint32_t keys_s, const uint4& x, uint32_t vj,
+                                         uint32_t* cnt) {
+  if constexpr (SMEM && sizeof(K) == 4 && !ONE) {
+    const uint32_t us[4] = {x.x, x.y, x.z, x.w};
+    uint32_t old[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                   : "=r"(old[e])
+                   : "r"(keys_s + (us[e] << 2)), "r"(0xffffffffu)
+                   : "memory");
+    uint32_t c = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) c += uint32_t(Range<K>::in_batch(K(old[e])) && us[e] < vj);
+    if (c) atomicAdd(cnt, c);
+  } else {
+    dec_key<K, SMEM, ONE>(keys, keys_s, x.x, vj, cnt);
+    dec_key<K, SMEM, ONE>(keys, keys_s, x.y, vj, cnt);
+    dec_key<K, SMEM, ONE>(keys, keys_s, x.z, vj, cnt);
+    dec_key<K, SMEM, ONE>(keys, keys_s, x.w, vj, cnt);
+  }
+}
+
 // timeline stamp (dg_peel_trace_*): lane 0 of every warp, armed window only.
 // The comparison on `dep` makes the stamp wait for a preceding load (it never
 // returns early: `first` is non-zero whenever a stamp is taken).
@@ -179,10 +207,7 @@ __device__ __forceinline__ void remove_row(const uint4* adj4, K* keys, uint32_t 
       if (t >= nq) break;
       const uint32_t e0 = t << 2;
       if (e0 >= head && e0 + 4 <= end) {
-        dec_key<K, SMEM, ONE>(keys, keys_s, x[k].x, vj, cnt);
-        dec_key<K, SMEM, ONE>(keys, keys_s, x[k].y, vj, cnt);
-        dec_key<K, SMEM, ONE>(keys, keys_s, x[k].z, vj, cnt);
-        dec_key<K, SMEM, ONE>(keys, keys_s, x[k].w, vj, cnt);
+        dec_quad<K, SMEM, ONE>(keys, keys_s, x[k], vj, cnt);
       } else {
         const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
 #pragma unroll
