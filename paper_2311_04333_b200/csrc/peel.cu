@@ -370,18 +370,16 @@ KeyRange key_range(const dg_graph& g, const uint64_t* d_loads) {
 }
 
 // Cluster variant: returns false when no cluster configuration fits.
-template <int CS>
-bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
-                    uint32_t* d_perm, uint64_t* d_raw, unsigned long long* d_batches) {
+template <int CS, int PT>
+bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
+                       uint32_t sh, uint32_t* d_perm, uint64_t* d_raw,
+                       unsigned long long* d_batches) {
   const uint64_t n = g.n;
-  uint32_t sh = 10;  // NC = 2^sh >= PT ids per CTA
-  while ((uint64_t(CS) << sh) < n) ++sh;
-  if (sh > 15) return false;  // <= 32 keys per thread (the S1 match mask)
   const bool offs32 = 2 * g.m < 0xffffffffULL;
   bool offs_smem = offs32 && peelc::smem_bytes(sh, true) <= kSmemCap;
   if (!offs_smem && peelc::smem_bytes(sh, false) > kSmemCap) return false;
   const size_t smem = peelc::smem_bytes(sh, offs_smem);
-  auto kern = peelc::k_peel_cluster<CS>;
+  auto kern = peelc::k_peel_cluster<CS, PT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess) {
     cudaGetLastError();
@@ -395,7 +393,7 @@ bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, b
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS);
-  cfg.blockDim = dim3(peelc::PT);
+  cfg.blockDim = dim3(PT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream();
   cudaLaunchAttribute attr[1];
@@ -413,11 +411,31 @@ bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, b
   // raw charges are accumulated with atomics (see peel_cluster.cuh)
   DG_CUDA(cudaMemsetAsync(d_raw, 0, n * sizeof(uint64_t), stream()));
   peelc::Args a{g.offs.get(), g.adj.get(), uint32_t(n), d_loads, base, one ? 1 : 0,
-                sh, (1u << sh) / peelc::PT, offs_smem ? 1 : 0, d_perm, d_raw, d_batches,
+                sh, (1u << sh) / PT, offs_smem ? 1 : 0, d_perm, d_raw, d_batches,
                 peel_prof_buffer()};
   DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   count_launch();
   return true;
+}
+
+// CTA size by block size: 512 threads while a CTA owns at most 4K ids
+// (RMAT-22's 35K core: 4.18 vs 4.37 us per batch), 1024 beyond (RMAT-26's
+// 84K core: 16 ids per thread at 512 make the scan the bottleneck).
+// DG_CLUSTER_PT=512|1024 overrides (tuning).
+template <int CS>
+bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
+                    uint32_t* d_perm, uint64_t* d_raw, unsigned long long* d_batches) {
+  uint32_t sh = 9;  // NC = 2^sh ids per CTA
+  while ((uint64_t(CS) << sh) < g.n) ++sh;
+  int pt = sh <= 12 ? 512 : 1024;
+  if (const char* e = getenv("DG_CLUSTER_PT")) pt = atoi(e) == 512 ? 512 : 1024;
+  if (pt == 1024) sh = sh < 10 ? 10 : sh;
+  // <= 32 keys per thread (the S1 match mask)
+  if (pt == 512 && sh <= 14)
+    return launch_cluster_pt<CS, 512>(g, d_loads, base, one, sh, d_perm, d_raw, d_batches);
+  if (sh <= 15)
+    return launch_cluster_pt<CS, 1024>(g, d_loads, base, one, sh, d_perm, d_raw, d_batches);
+  return false;
 }
 
 void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,

@@ -47,9 +47,7 @@ namespace peelc {
 namespace cg = cooperative_groups;
 using peelk::Range;
 
-constexpr int PT = 1024;
-constexpr int NW = PT / 32;
-constexpr int UQ = 2;
+constexpr int MAXW = 32;  // warps per CTA at most (PT <= 1024)
 constexpr int SB = 32;  // staged (small) batch members
 
 struct Args {
@@ -84,13 +82,14 @@ struct Fixed {
   unsigned long long mbA[2], mbB[2];  // summaries / staged members, by parity
   Summary sum[2][16];                 // [parity][CTA rank]
   Member stage[2][SB];                // [parity][member]
-  uint32_t wmin[NW];
-  uint32_t wcnt[NW];
-  uint32_t wfirst[NW];
+  uint32_t wmin[MAXW];
+  uint32_t wcnt[MAXW];
+  uint32_t wfirst[MAXW];
   // warp -> member map over this CTA's warps for batches of b <= SB members:
   // wmap[b-1][w] = j | rank << 8 | nwj << 16 (j = w % b, rank = w / b,
-  // nwj = #warps serving member j)
-  uint32_t wmap[SB][NW];
+  // nwj = #warps serving member j); batches of more than NW members are
+  // removed as one flat quad range (remove_flat)
+  uint32_t wmap[MAXW][MAXW];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -127,7 +126,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 
 // row [oj, oj + dj) of member vj, quads [rk*32 + lane, ...) step nwj*32:
 // decrement the targets in this CTA's block [gbase, gbase + NC)
-template <bool ONE>
+template <bool ONE, int UQ>
 __device__ __forceinline__ void remove_local(const uint4* adj4, uint32_t keys_s, uint64_t oj,
                                              uint32_t dj, uint32_t vj, uint32_t rk, uint32_t nwj,
                                              uint32_t lane, uint32_t gbase, uint32_t NC,
@@ -176,8 +175,71 @@ __device__ __forceinline__ void remove_local(const uint4* adj4, uint32_t keys_s,
   }
 }
 
-template <int CS>
+// removal of a multi-member batch (bs <= 32) as ONE flat range of 16-byte
+// quads: the members' rows concatenated (lane j of every warp holds member
+// j: id, degree, row start), 2 quads per thread per round over the CTA, each
+// quad's member found by a 5-step binary search over the lanes' prefix
+// sums.  Every thread gets the same share however the batch's degrees vary.
+template <int PT>
+__device__ __forceinline__ void remove_flat(const uint4* adj4, uint32_t keys_s, uint32_t bs,
+                                            uint32_t mv, uint32_t mdeg, uint64_t mr0,
+                                            uint32_t w, uint32_t lane, uint32_t gbase,
+                                            uint32_t NC, unsigned long long* rawpos) {
+  const uint32_t nq = lane < bs ? (uint32_t(mr0 & 3) + mdeg + 3) >> 2 : 0u;
+  const uint32_t incl = warp_incl_scan(nq), excl = incl - nq;
+  const uint32_t totq = __shfl_sync(~0u, incl, 31);
+  for (uint32_t base = w * 32; base < totq; base += 2 * PT) {
+    uint4 x[2];
+    uint32_t m[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t t = base + k * PT + lane;
+      uint32_t lo = 0, hi = bs - 1;  // largest member with excl <= t
+#pragma unroll
+      for (int it = 0; it < 5; ++it) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        const uint32_t e = __shfl_sync(~0u, excl, mid);
+        if (e <= t) lo = mid; else hi = mid - 1;
+      }
+      m[k] = lo;
+      const uint64_t r0 = __shfl_sync(~0u, mr0, lo);
+      const uint32_t ex = __shfl_sync(~0u, excl, lo);
+      if (t < totq) x[k] = __ldg(adj4 + (r0 >> 2) + (t - ex));
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t t = base + k * PT + lane;
+      const uint64_t r0 = __shfl_sync(~0u, mr0, m[k]);
+      const uint32_t d = __shfl_sync(~0u, mdeg, m[k]), v = __shfl_sync(~0u, mv, m[k]);
+      const uint32_t ex = __shfl_sync(~0u, excl, m[k]);
+      if (t >= totq) continue;
+      const uint64_t q = (r0 >> 2) + (t - ex);
+      const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+      uint32_t old[4];
+      bool ok[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t pp = (q << 2) + e;
+        ok[e] = pp >= r0 && pp < r0 + d && us[e] - gbase < NC;
+        old[e] = 0;
+        if (ok[e])
+          asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                       : "=r"(old[e])
+                       : "r"(keys_s + ((us[e] - gbase) << 2)), "r"(0xffffffffu)
+                       : "memory");
+      }
+      unsigned long long c = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) c += (ok[e] && Range<uint32_t>::in_batch(old[e]) && us[e] < v);
+      if (c) atomicAdd(rawpos + m[k], 0ULL - c);
+    }
+  }
+}
+
+template <int CS, int PT>
 __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
+  constexpr uint32_t NW = PT / 32;
+  constexpr int UQ = PT >= 1024 ? 2 : 4;  // quads in flight per thread (64 registers at 1024)
   static_assert(CS <= 16, "summary slots");
   using R = Range<uint32_t>;
   cg::cluster_group cl = cg::this_cluster();
@@ -207,7 +269,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     }
   }
   if (a.offs_smem && tid == 0) soffs[NC] = uint32_t(a.offs[min(n, gbase + NC)]);
-  for (uint32_t e = tid; e < SB * NW; e += PT) {
+  for (uint32_t e = tid; e < NW * NW; e += PT) {
     const uint32_t b = e / NW + 1, ww = e % NW;
     const uint32_t jj = ww % b;
     s.wmap[b - 1][ww] = jj | ((ww / b) << 8) | (((NW - 1 - jj) / b + 1) << 16);
@@ -269,7 +331,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     if (tid == 0) mbar_expect(mbA, CS * uint32_t(sizeof(Summary)));
     __syncthreads();
     if (w == 0) {  // CTA summary, pushed to every CTA (lane q -> CTA q)
-      const uint32_t x = s.wmin[lane];
+      const uint32_t x = lane < NW ? s.wmin[lane] : R::DEAD;
       const uint32_t cm = __reduce_min_sync(~0u, x);
       const uint32_t ccnt = __reduce_add_sync(~0u, x == cm ? s.wcnt[lane] : 0u);
       const uint32_t fw = __ffs(__ballot_sync(~0u, x == cm)) - 1;
@@ -318,11 +380,6 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       // ---- simple batch: owner lane L (CTA L) holds member #(owners below L)
       ++nsimple;
       const uint32_t rkl = __popc(ownmask & ((1u << lane) - 1u));
-      const uint32_t wm3 = s.wmap[bs - 1][w];
-      const uint32_t j = wm3 & 0xffu, rk = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
-      const uint32_t lj = __ffs(__ballot_sync(~0u, own && rkl == j)) - 1;
-      const uint32_t vj = __shfl_sync(~0u, rfirst, lj), dj = __shfl_sync(~0u, rdeg, lj);
-      const uint64_t oj = __shfl_sync(~0u, rr0, lj);
       // my CTA's member (if any): every warp marks it before its own
       // decrements (a later mark by another warp only rewrites a batch key)
       const uint32_t mrk = __popc(ownmask & ((1u << rank) - 1u));
@@ -339,11 +396,23 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         if (bs != 1 && mv - gbase - lo < c) marked = true;
       }
       __syncwarp();
-      unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
-      if (bs == 1)
-        remove_local<true>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
-      else
-        remove_local<false>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
+      if (bs <= NW) {
+        const uint32_t wm3 = s.wmap[bs - 1][w];
+        const uint32_t j = wm3 & 0xffu, rk = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
+        const uint32_t lj = __ffs(__ballot_sync(~0u, own && rkl == j)) - 1;
+        const uint32_t vj = __shfl_sync(~0u, rfirst, lj), dj = __shfl_sync(~0u, rdeg, lj);
+        const uint64_t oj = __shfl_sync(~0u, rr0, lj);
+        unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
+        if (bs == 1)
+          remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
+        else
+          remove_local<false, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
+      } else if constexpr (NW < 32) {  // lane j <- member j (the owner lane of rank j)
+        const uint32_t lj = (lane < bs ? __fns(ownmask, 0, int(lane) + 1) : 0u) & 31u;
+        remove_flat<PT>(adj4, keys_s, bs, __shfl_sync(~0u, rfirst, lj), __shfl_sync(~0u, rdeg, lj),
+                    __shfl_sync(~0u, rr0, lj), w, lane, gbase, NC,
+                    reinterpret_cast<unsigned long long*>(&a.raw[pos]));
+      }
       if (P) {
         const long long t = clock64();
         c2 += t - tm;
@@ -355,7 +424,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       if (tid == 0 && bs <= SB) mbar_expect(mbB, bs * uint32_t(sizeof(Member)));
       if (((ownmask >> rank) & 1u) && wm == gmin) {  // this warp owns part of the batch
         const uint32_t cta_off = __reduce_add_sync(~0u, (lane < rank && own) ? rcnt : 0u);
-        const uint32_t xw = s.wmin[lane];
+        const uint32_t xw = lane < NW ? s.wmin[lane] : R::DEAD;
         const uint32_t woff = __reduce_add_sync(~0u, (lane < w && xw == gmin) ? s.wcnt[lane] : 0u);
         const bool mine = lmin == gmin && lcnt;
         const uint32_t mm = __ballot_sync(~0u, mine);
@@ -399,12 +468,19 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           c2 += t - tm;
           tm = t;
         }
-        const uint32_t wm3 = s.wmap[bs - 1][w];
-        const uint32_t j = wm3 & 0xffu, rk = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
-        const Member& mj = s.stage[par][j];
-        remove_local<false>(adj4, keys_s, uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32), mj.deg,
-                            mj.v, rk, nwj, lane, gbase, NC,
-                            reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
+        if (bs <= NW) {
+          const uint32_t wm3 = s.wmap[bs - 1][w];
+          const uint32_t j = wm3 & 0xffu;
+          const Member& mj = s.stage[par][j];
+          remove_local<false, UQ>(adj4, keys_s, uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32), mj.deg,
+                              mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NC,
+                              reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
+        } else if constexpr (NW < SB) {
+          Member mj = {0u, 0u, 0u, 0u};
+          if (lane < bs) mj = s.stage[par][lane];
+          remove_flat<PT>(adj4, keys_s, bs, mj.v, mj.deg, uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32),
+                      w, lane, gbase, NC, reinterpret_cast<unsigned long long*>(&a.raw[pos]));
+        }
         __syncthreads();
       } else {
         // large batch: CTA r takes members j = r, r + CS, ...; its warps

@@ -25,4 +25,8 @@ for T in Ts:
     print(f"T={T} CS={prof[7]} n={it.n} batches={nb} simple={prof[4]} order={it.order_ms:.3f} ms "
           f"({1e3 * it.order_ms / nb:.2f} us/batch) cycles/batch S1={prof[0] / nb:.0f} "
           f"S2={prof[1] / nb:.0f} S3={prof[2] / nb:.0f}")
+    if os.environ.get("DG_STAMPS"):
+        ng = max(1, nb - int(prof[4]))
+        print("  general batches: cycles per batch (owner loop, CTA barrier, member wait, removal):",
+              [round(float(prof[12 + k]) / ng) for k in range(4)])
 dg.set_peel_mode(0)
