@@ -370,6 +370,13 @@ def test_peel_queue_paths(dg, orc, mode):
     cases.append((gu, gv, rng.integers(0, 64, 4000).astype(np.uint64)))
     ru, rv = orc.gen_rmat(14, 8 << 14, 5)
     cases.append((ru, rv, None))
+    # 24 twins (identical neighbourhoods: the same 40 hubs of a 20K-vertex
+    # G(n,p)) tie in every batch that reaches them: a tie group between the
+    # cluster kernel's warp count and its staging limit (flat removal)
+    bu, bv = orc.gen_gnp(20000, 1, 3)
+    hubs = np.arange(0, 20000, 500, dtype=np.uint64)
+    tw = np.repeat(np.arange(20000, 20024, dtype=np.uint64), len(hubs))
+    cases.append((np.concatenate([bu, tw]), np.concatenate([bv, np.tile(hubs, 24)]), None))
     dg.set_peel_mode(mode)
     try:
         for u, v, loads in cases:
