@@ -271,14 +271,20 @@ bool peel_trace_armed() {
   return g_peel_trace_armed[d];
 }
 
-template <class K, bool SMEM, bool OFFS, int VQ, bool TR = false>
+template <class K, bool SMEM, bool OFFS, int VQ, bool TR = false, bool SMALL = false>
 void launch_peel(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
                  uint32_t chunk, uint32_t* d_perm, uint64_t* d_raw,
                  unsigned long long* d_batches) {
+  // just enough warps to hold the keys: idle warps still issue the
+  // per-warp table reduction of every batch (RMAT-22's 9.1K core: 24 warps
+  // instead of 32, 1.95 -> 1.85 us per batch)
+  const uint64_t wkeys = uint64_t(chunk) * 32;
+  const uint32_t nt = uint32_t(
+      std::min<uint64_t>(peelk::PT, std::max<uint64_t>(1, (g.n + wkeys - 1) / wkeys) * 32));
   DevBuf<K> gk;
-  if (!SMEM) gk.alloc(size_t(chunk) * peelk::PT);
-  const size_t smem = peelk::smem_bytes<K, OFFS>(chunk, SMEM);
-  auto kern = peelk::k_peel<K, SMEM, OFFS, VQ, TR>;
+  if (!SMEM) gk.alloc(size_t(chunk) * nt);
+  const size_t smem = peelk::smem_bytes<K, OFFS>(chunk, SMEM, nt);
+  auto kern = peelk::k_peel<K, SMEM, OFFS, VQ, TR, SMALL ? 768 : peelk::PT>;
   if (TR)  // timeline of this launch only
     DG_CUDA(cudaMemsetAsync(peel_prof_buffer() + 16, 0, kPeelTraceWords * 8, stream()));
   DG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -286,7 +292,7 @@ void launch_peel(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool
                    gk.get(), chunk, d_perm, d_raw, d_batches, peel_prof_buffer()};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(1);
-  cfg.blockDim = dim3(peelk::PT);
+  cfg.blockDim = dim3(nt);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream();
   DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
@@ -303,6 +309,9 @@ bool launch_vec(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool 
     if (OFFS && peel_trace_armed())                                                      \
       launch_peel<uint32_t, true, OFFS, V, OFFS>(g, d_loads, base, one, 4 * V, d_perm,   \
                                                  d_raw, d_batches);                      \
+    else if (g.n <= 768ULL * V * 4)                                                      \
+      launch_peel<uint32_t, true, OFFS, V, false, true>(g, d_loads, base, one, 4 * V,    \
+                                                        d_perm, d_raw, d_batches);       \
     else                                                                                 \
       launch_peel<uint32_t, true, OFFS, V>(g, d_loads, base, one, 4 * V, d_perm, d_raw,  \
                                            d_batches);                                   \

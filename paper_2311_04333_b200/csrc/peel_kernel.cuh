@@ -258,11 +258,15 @@ __device__ __forceinline__ void chunk_min_count(const K* keys, uint32_t lo, uint
 }
 
 // TR: timeline + cycle counters variant (dg_peel_trace_*, dg_peel_profile)
-template <class K, bool SMEM, bool OFFS, int VQ, bool TR>
-__global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
+// LB: launch bound (the largest NT launched with this instantiation): 768
+// leaves 85 registers per thread instead of 64
+template <class K, bool SMEM, bool OFFS, int VQ, bool TR, int LB = PT>
+__global__ void __launch_bounds__(LB, 1) k_peel(Args<K> a) {
   using R = Range<K>;
   extern __shared__ __align__(16) unsigned char raw_smem[];
-  const uint32_t npad = a.chunk * PT;
+  // NT threads (<= PT): just enough warps to hold the keys (peel.cu)
+  const uint32_t NT = blockDim.x, NW = NT >> 5;
+  const uint32_t npad = a.chunk * NT;
   size_t o = 0;
   K* keys = a.gkeys;
   if (SMEM) {
@@ -277,7 +281,6 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
   const uint32_t n = a.n, c = VQ > 0 ? uint32_t(4 * VQ) : a.chunk, lo = tid * c, hi = lo + c;
-  constexpr uint32_t NW = PT / 32;
 
   for (uint32_t i = lo; i < hi; ++i) {
     if (i < n) {
@@ -289,12 +292,12 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
     }
   }
   if (OFFS && tid == 0) soffs[n] = uint32_t(a.offs[n]);
-  for (uint32_t e = tid; e < NW * NW; e += PT) {
+  for (uint32_t e = tid; e < NW * NW; e += NT) {
     const uint32_t b = e / NW + 1, ww = e % NW;
     const uint32_t jj = ww % b;
     s.wmap[b - 1][ww] = jj | ((ww / b) << 8) | (((NW - 1 - jj) / b + 1) << 16);
   }
-  if (tid < 64) (&s.cnt2[0][0])[tid] = 0;
+  for (uint32_t e = tid; e < 64; e += NT) (&s.cnt2[0][0])[e] = 0;
   __syncthreads();
 
   const unsigned long long tr_first = TR && a.prof ? a.prof[15] : 0;  // 0: timeline disarmed
@@ -314,8 +317,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
     PK_STAMP(0, s.wcnt[(w + 1) & 31]);
     // ---- deferred raw charges of the previous batch (last warp: usually
     // padding keys only, the first to finish S1)
-    if (tid >= PT - 32 && tid - (PT - 32) < pend_n) {
-      const uint32_t t = tid - (PT - 32);
+    if (tid >= NT - 32 && tid - (NT - 32) < pend_n) {
+      const uint32_t t = tid - (NT - 32);
       a.raw[pend_pos + t] = uint64_t(pend_key) - pend_cnt[t];
       if (pend_reset) pend_cnt[t] = 0;
     }
@@ -483,7 +486,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
             // a single-vertex batch has no same-batch arcs: mark it dead at once
             keys[i] = bs == 1 ? R::DEAD : R::BATCH;
             marked = bs != 1;
-            if (my < PT) {
+            if (my < NT) {
               uint64_t q0, q1;
               if (OFFS) {
                 q0 = soffs[i];
@@ -534,9 +537,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
         pend_cnt = s.cnt;
         pend_reset = false;
       } else {
-        // ---- S3, large batch: slices of PT members with a CTA scan
-        for (uint32_t s0 = 0; s0 < bs; s0 += PT) {
-          const uint32_t sl = min(uint32_t(PT), bs - s0);
+        // ---- S3, large batch: slices of NT members with a CTA scan
+        for (uint32_t s0 = 0; s0 < bs; s0 += NT) {
+          const uint32_t sl = min(uint32_t(NT), bs - s0);
           if (s0 > 0 && tid < sl) {  // beyond the staged first slice
             const uint32_t v = a.perm[pos + s0 + tid];
             const uint64_t q0 = a.offs[v], q1 = a.offs[v + 1];
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
           const uint64_t ex = block_excl_scan(d, s.ws, &tot);
           s.pre[tid] = ex + d;
           __syncthreads();
-          for (uint64_t b0 = uint64_t(w) * 32 * U; b0 < tot; b0 += uint64_t(PT) * U) {
+          for (uint64_t b0 = uint64_t(w) * 32 * U; b0 < tot; b0 += uint64_t(NT) * U) {
             uint32_t u[U], bb[U];
 #pragma unroll
             for (int jx = 0; jx < U; ++jx) {
@@ -599,8 +602,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
     ++nbat;
   }
 #undef PK_STAMP
-  if (tid >= PT - 32 && tid - (PT - 32) < pend_n) {
-    const uint32_t t = tid - (PT - 32);
+  if (tid >= NT - 32 && tid - (NT - 32) < pend_n) {
+    const uint32_t t = tid - (NT - 32);
     a.raw[pend_pos + t] = uint64_t(pend_key) - pend_cnt[t];
   }
   if (tid == 0) {
@@ -620,8 +623,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel(Args<K> a) {
 }
 
 template <class K, bool OFFS>
-size_t smem_bytes(uint32_t chunk, bool in_smem) {
-  const size_t npad = size_t(chunk) * PT;
+size_t smem_bytes(uint32_t chunk, bool in_smem, uint32_t nt = PT) {
+  const size_t npad = size_t(chunk) * nt;
   size_t b = in_smem ? ((npad * sizeof(K) + 15) & ~size_t(15)) : 0;
   if (OFFS) b += ((npad + 1) * 4 + 15) & ~size_t(15);
   return b + sizeof(Fixed);
