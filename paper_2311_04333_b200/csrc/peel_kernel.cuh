@@ -39,6 +39,8 @@
 //   raw charges of the batch are written to global at the next S1.
 #pragma once
 
+#include <type_traits>
+
 namespace dgb {
 namespace peelk {
 
@@ -235,16 +237,22 @@ __device__ __forceinline__ void chunk_min_count(const K* keys, uint32_t lo, uint
       const uint4 v = kv[q];
       m = min(min(m, min(v.x, v.y)), min(v.z, v.w));
     }
-    uint64_t mask = 0;
+    using M = std::conditional_t<(4 * VQ <= 32), uint32_t, uint64_t>;  // 32-bit ops when they fit
+    M mask = 0;
 #pragma unroll
     for (int q = 0; q < VQ; ++q) {
       const uint4 v = kv[q];
-      mask |= uint64_t((v.x == m) | ((v.y == m) << 1) | ((v.z == m) << 2) | ((v.w == m) << 3))
+      mask |= M((v.x == m) | ((v.y == m) << 1) | ((v.z == m) << 2) | ((v.w == m) << 3))
               << (4 * q);
     }
     lmin = K(m);
-    lcnt = uint32_t(__popcll(mask));
-    lfirst = lo + uint32_t(__ffsll(mask)) - 1;
+    if constexpr (sizeof(M) == 4) {
+      lcnt = uint32_t(__popc(mask));
+      lfirst = lo + uint32_t(__ffs(mask)) - 1;
+    } else {
+      lcnt = uint32_t(__popcll(mask));
+      lfirst = lo + uint32_t(__ffsll(mask)) - 1;
+    }
   } else {
     K m = K(~K(0));
     for (uint32_t i = lo; i < lo + c; ++i) m = min(m, keys[i]);
@@ -347,36 +355,86 @@ __global__ void __launch_bounds__(LB, 1) k_peel(Args<K> a) {
       marked = false;
     }
     // ---- S1
+    // COOP (u32 keys + offsets in shared memory, chunks of 20..32 keys): each
+    // thread only takes its chunk minimum; the warp then counts the keys at
+    // its minimum by testing the chunk of the lane(s) holding it, one key per
+    // lane (one load + one ballot per candidate lane, usually one), instead
+    // of every thread building a match mask of its chunk.  lcnt is then 1 for
+    // any alive chunk and recomputed exactly where the general path needs it.
+    // RMAT-24's 12.9K core (20 keys per thread): 2.52 -> 2.43 us per batch;
+    // with 12 keys the longer dependent chain costs more than the mask
+    // (RMAT-22's 9.1K core: 1.77 -> 1.81), so 12-key chunks keep the mask.
+    constexpr bool COOP = VQ >= 5 && sizeof(K) == 4 && OFFS && 4 * VQ <= 32;
     K lmin = R::DEAD;
     uint32_t lcnt = 0, lfirst = lo;
-    if (lo < n) chunk_min_count<VQ>(keys, lo, c, lmin, lcnt, lfirst);  // padding: skip
-    if (!R::alive(lmin)) {  // nothing alive in my chunk
-      lmin = R::DEAD;
-      lcnt = 0;
-      lfirst = lo;
-    }
-    // row bounds of my first minimum: staged offsets, or (without them) an
-    // early L2 load whose round trip overlaps barrier A
     uint64_t r0 = 0, r1 = 0;
-    if (OFFS) {
-      r0 = soffs[lfirst];
-      r1 = soffs[lfirst + 1];
-    } else if (R::alive(lmin)) {
-      r0 = a.offs[lfirst];
-      r1 = a.offs[lfirst + 1];
+    if constexpr (COOP) {
+      if (lo < n) {
+        const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
+        uint32_t m = 0xffffffffu;
+#pragma unroll
+        for (int q = 0; q < VQ; ++q) {
+          const uint4 v = kv[q];
+          m = min(min(m, min(v.x, v.y)), min(v.z, v.w));
+        }
+        lmin = K(m);
+      }
+      if (!R::alive(lmin)) lmin = R::DEAD;
+      lcnt = R::alive(lmin) ? 1u : 0u;
+    } else {
+      if (lo < n) chunk_min_count<VQ>(keys, lo, c, lmin, lcnt, lfirst);  // padding: skip
+      if (!R::alive(lmin)) {  // nothing alive in my chunk
+        lmin = R::DEAD;
+        lcnt = 0;
+        lfirst = lo;
+      }
+      // row bounds of my first minimum: staged offsets, or (without them) an
+      // early L2 load whose round trip overlaps barrier A
+      if (OFFS) {
+        r0 = soffs[lfirst];
+        r1 = soffs[lfirst + 1];
+      } else if (R::alive(lmin)) {
+        r0 = a.offs[lfirst];
+        r1 = a.offs[lfirst + 1];
+      }
     }
     const K wm = wmin_key(lmin);
-    const uint32_t wc = __reduce_add_sync(~0u, lmin == wm ? lcnt : 0u);
-    if (lane == 0) {
-      s.wmin[w] = uint64_t(wm);
-      s.wcnt[w] = wc;
-    }
-    if (OFFS) {  // the warp's candidate: first lane at the warp minimum
-      const uint32_t fl = __ffs(__ballot_sync(~0u, lmin == wm)) - 1;
-      if (lane == fl) {
-        s.wfirst[w] = lfirst;
-        s.wr0[w] = uint32_t(r0);
-        s.wdeg[w] = uint32_t(r1 - r0);
+    if constexpr (COOP) {
+      uint32_t wc = 0, wf = 0;
+      if (R::alive(wm)) {  // warp-uniform
+        uint32_t cm = __ballot_sync(~0u, lmin == wm);
+        const uint32_t wbase = w * 32 * c;
+        bool first = true;
+        while (cm) {
+          const uint32_t L = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const uint32_t k = lane < c ? uint32_t(keys[wbase + L * c + lane]) : uint32_t(R::DEAD);
+          const uint32_t eq = __ballot_sync(~0u, k == uint32_t(wm));
+          if (first) wf = wbase + L * c + __ffs(eq) - 1, first = false;
+          wc += __popc(eq);
+        }
+      }
+      if (lane == 0) {
+        const uint32_t q0 = soffs[wf], q1 = soffs[wf + 1];
+        s.wmin[w] = uint64_t(wm);
+        s.wcnt[w] = wc;
+        s.wfirst[w] = wf;
+        s.wr0[w] = q0;
+        s.wdeg[w] = q1 - q0;
+      }
+    } else {
+      const uint32_t wc = __reduce_add_sync(~0u, lmin == wm ? lcnt : 0u);
+      if (lane == 0) {
+        s.wmin[w] = uint64_t(wm);
+        s.wcnt[w] = wc;
+      }
+      if (OFFS) {  // the warp's candidate: first lane at the warp minimum
+        const uint32_t fl = __ffs(__ballot_sync(~0u, lmin == wm)) - 1;
+        if (lane == fl) {
+          s.wfirst[w] = lfirst;
+          s.wr0[w] = uint32_t(r0);
+          s.wdeg[w] = uint32_t(r1 - r0);
+        }
       }
     }
     PK_STAMP(1, 0);
@@ -447,6 +505,20 @@ __global__ void __launch_bounds__(LB, 1) k_peel(Args<K> a) {
       // ---- general batch: owners write the batch in ascending id and stage
       // (v, row offset, degree) for the CTA
       if (wm == gmin) {
+        if constexpr (COOP) {  // exact count of my chunk's keys at gmin
+          if (lmin == gmin) {
+            const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
+            uint32_t b = 0;
+#pragma unroll
+            for (int q = 0; q < VQ; ++q) {
+              const uint4 v = kv[q];
+              b |= uint32_t((v.x == gmin) | ((v.y == gmin) << 1) | ((v.z == gmin) << 2) |
+                            ((v.w == gmin) << 3))
+                   << (4 * q);
+            }
+            lcnt = __popc(b);
+          }
+        }
         const uint32_t woff = __reduce_add_sync(~0u, lane < w ? cc : 0u);
         const uint32_t mm = __ballot_sync(~0u, mine);
         uint32_t my = woff;
