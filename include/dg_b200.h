@@ -308,8 +308,9 @@ dg_status dg_peel_trace_read(uint64_t out[8 * 32 * 12]);
  * barriers; #level advances; #overflow collects. */
 dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]);  /* + per-round trace */
 /* Tuning / testing knob for the Greedy++ ordering kernel: 0 automatic (batch
- * mode: the candidate-list kernel for cores above 16K vertices whose keys fit
- * one SM; then the scanning single-CTA kernel; then a thread-block cluster), 1 scanning
+ * mode: the thread-block cluster kernel for cores above 16K vertices, the
+ * candidate-list kernel when no cluster fits; then the scanning single-CTA
+ * kernel; then a thread-block cluster), 1 scanning
  * single-CTA kernel only, 2 cluster (16 or 8 CTAs) whenever it fits, 3
  * candidate-list kernel whenever it fits.  Results are identical in every
  * mode. */

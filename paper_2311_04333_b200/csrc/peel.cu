@@ -378,6 +378,31 @@ KeyRange key_range(const dg_graph& g, const uint64_t* d_loads) {
   return kr;
 }
 
+// Per-row CTA slices for the cluster kernel: seg[v*(CS+1) + r] = index
+// inside row v of its first neighbour >= r << sh (rows ascend), one thread
+// per (row, r) by binary search.
+template <int CS>
+__global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t n, uint32_t sh,
+                            uint32_t* seg) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * (CS + 1);
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t v = i / (CS + 1);
+    const uint32_t r = uint32_t(i % (CS + 1));
+    const uint64_t o0 = offs[v];
+    uint32_t lo = 0, hi = uint32_t(offs[v + 1] - o0);
+    if (r == 0) {
+      hi = 0;
+    } else if (r < CS) {
+      const uint32_t x = r << sh;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (adj[o0 + mid] < x) lo = mid + 1; else hi = mid;
+      }
+    }
+    seg[i] = hi;
+  }
+}
+
 // Cluster variant: returns false when no cluster configuration fits.
 template <int CS, int PT>
 bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
@@ -419,8 +444,12 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
   }
   // raw charges are accumulated with atomics (see peel_cluster.cuh)
   DG_CUDA(cudaMemsetAsync(d_raw, 0, n * sizeof(uint64_t), stream()));
+  DevBuf<uint32_t> seg(n * (CS + 1));
+  k_seg_table<CS><<<grid_for(n * (CS + 1), 256), 256, 0, stream()>>>(g.offs.get(), g.adj.get(), n,
+                                                                      sh, seg.get());
+  DG_CHECK_LAUNCH();
   peelc::Args a{g.offs.get(), g.adj.get(), uint32_t(n), d_loads, base, one ? 1 : 0,
-                sh, (1u << sh) / PT, offs_smem ? 1 : 0, d_perm, d_raw, d_batches,
+                sh, (1u << sh) / PT, offs_smem ? 1 : 0, d_perm, d_raw, seg.get(), d_batches,
                 peel_prof_buffer()};
   DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   count_launch();
@@ -471,9 +500,13 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
   // when the core's keys do not fit one SM, a 16- (or 8-) CTA cluster with the
   // keys spread over distributed shared memory; then the u64 / global-key
   // single-CTA fallbacks.  dg_set_peel_mode can force either kernel.
-  // batch mode: the candidate-list kernel (peel_queue.cuh) for cores above
-  // kQueueMinN vertices (RMAT-22's 35K core: 4.9 vs 5.9 us per batch; on the
-  // 9.1K core the scanning kernel is ahead, 1.99 vs 2.15 us)
+  // batch mode beyond kQueueMinN: the cluster kernel (RMAT-22's 35K core
+  // 3.52 vs 4.22 us per batch for the candidate-list kernel, RMAT-26's 17.9K
+  // core 2.98 vs 3.20), the candidate-list kernel when no cluster fits
+  if (k32 && !one_at_a_time && g_peel_mode == 0 && g.n > kQueueMinN) {
+    if (launch_cluster<16>(g, d_loads, base, false, d_perm, d_raw, d_batches)) return;
+    if (launch_cluster<8>(g, d_loads, base, false, d_perm, d_raw, d_batches)) return;
+  }
   if (k32 && !one_at_a_time &&
       ((g_peel_mode == 0 && g.n > kQueueMinN) || g_peel_mode == 3)) {
     if (offs32 && launch_queue<true>(g, d_loads, base, vq, d_perm, d_raw, d_batches)) return;

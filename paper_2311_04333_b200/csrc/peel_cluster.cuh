@@ -49,6 +49,11 @@ using peelk::Range;
 
 constexpr int MAXW = 32;  // warps per CTA at most (PT <= 1024)
 constexpr int SB = 32;  // staged (small) batch members
+#ifndef DG_SLICE_MIN
+#define DG_SLICE_MIN 2048
+#endif
+// simple batches read only the CTA's slice of rows at least this long
+constexpr uint32_t kSliceMin = DG_SLICE_MIN;
 
 struct Args {
   const uint64_t* offs;
@@ -62,6 +67,9 @@ struct Args {
   int offs_smem;   // row offsets staged in shared memory (u32)
   uint32_t* perm;
   uint64_t* raw;   // zeroed by the launcher
+  // seg[v*(CS+1) + r]: offset inside row v of its first neighbour owned by
+  // CTA r (rows ascend, so CTA r's targets are [seg[r], seg[r+1]))
+  const uint32_t* seg;
   unsigned long long* batches;
   unsigned long long* prof;  // [8] rank-0 thread-0 cycles: S1, S2, S3, batches, simple
 };
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
 
   uint32_t removed = 0, pos = 0, useB = 0;  // useB bit k: phase parity of mbB[k]
   bool marked = false;  // my chunk holds BATCH marks of the previous batch
-  unsigned long long nbat = 0, nsimple = 0;
+  unsigned long long nbat = 0, nsimple = 0, nlarge = 0, clarge = 0, mlarge = 0;
   const bool P = rank == 0 && tid == 0;
   long long c1 = 0, c2 = 0, c3 = 0, tm = clock64();
   while (removed < n) {
@@ -400,8 +408,15 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         const uint32_t wm3 = s.wmap[bs - 1][w];
         const uint32_t j = wm3 & 0xffu, rk = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
         const uint32_t lj = __ffs(__ballot_sync(~0u, own && rkl == j)) - 1;
-        const uint32_t vj = __shfl_sync(~0u, rfirst, lj), dj = __shfl_sync(~0u, rdeg, lj);
-        const uint64_t oj = __shfl_sync(~0u, rr0, lj);
+        const uint32_t vj = __shfl_sync(~0u, rfirst, lj);
+        uint32_t dj = __shfl_sync(~0u, rdeg, lj);
+        uint64_t oj = __shfl_sync(~0u, rr0, lj);
+        if (dj >= kSliceMin) {  // long row: only this CTA's slice (one more L2 round trip)
+          const uint32_t* sg = a.seg + size_t(vj) * (CS + 1) + rank;
+          const uint32_t s0 = sg[0], s1 = sg[1];
+          oj += s0;
+          dj = s1 - s0;
+        }
         unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
         if (bs == 1)
           remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
@@ -472,33 +487,42 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           const uint32_t wm3 = s.wmap[bs - 1][w];
           const uint32_t j = wm3 & 0xffu;
           const Member& mj = s.stage[par][j];
-          remove_local<false, UQ>(adj4, keys_s, uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32), mj.deg,
-                              mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NC,
-                              reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
+          // only this CTA's slice of the member's row
+          const uint32_t* sg = a.seg + size_t(mj.v) * (CS + 1) + rank;
+          const uint32_t s0 = sg[0], s1 = sg[1];
+          remove_local<false, UQ>(adj4, keys_s,
+                                  (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, s1 - s0,
+                                  mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NC,
+                                  reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
         } else if constexpr (NW < SB) {
           Member mj = {0u, 0u, 0u, 0u};
-          if (lane < bs) mj = s.stage[par][lane];
-          remove_flat<PT>(adj4, keys_s, bs, mj.v, mj.deg, uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32),
-                      w, lane, gbase, NC, reinterpret_cast<unsigned long long*>(&a.raw[pos]));
+          uint32_t s0 = 0, s1 = 0;
+          if (lane < bs) {
+            mj = s.stage[par][lane];
+            const uint32_t* sg = a.seg + size_t(mj.v) * (CS + 1) + rank;
+            s0 = sg[0];
+            s1 = sg[1];
+          }
+          remove_flat<PT>(adj4, keys_s, bs, mj.v, s1 - s0,
+                          (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, w, lane, gbase, NC,
+                          reinterpret_cast<unsigned long long*>(&a.raw[pos]));
         }
         __syncthreads();
       } else {
-        // large batch: CTA r takes members j = r, r + CS, ...; its warps
-        // split a row and decrement through DSMEM on the owner CTA
+        // large batch: every warp takes members w, w + NW, ... and applies
+        // the decrements of its slice of their rows to this CTA's keys
+        const long long tl0 = P ? clock64() : 0;
         cl.sync();  // perm and every batch mark written
-        const uint32_t msk = NC - 1;
-        for (uint32_t j = rank; j < bs; j += CS) {
+        for (uint32_t j = w; j < bs; j += NW) {
           const uint32_t vj = a.perm[pos + j];
-          const uint64_t oj = a.offs[vj], ej = a.offs[vj + 1];
-          for (uint64_t p = oj + tid; p < ej; p += PT) {
-            const uint32_t u = a.adj[p];
-            uint32_t* rk = cl.map_shared_rank(keys, u >> a.sh) + (u & msk);
-            const uint32_t old = atomicAdd(rk, 0xffffffffu);
-            if (R::in_batch(old) && u < vj)
-              atomicAdd(reinterpret_cast<unsigned long long*>(&a.raw[pos + j]), ~0ULL);
-          }
+          const uint64_t oj = a.offs[vj];
+          const uint32_t* sg = a.seg + size_t(vj) * (CS + 1) + rank;
+          const uint32_t s0 = sg[0], s1 = sg[1];
+          remove_local<false, UQ>(adj4, keys_s, oj + s0, s1 - s0, vj, 0, 1, lane, gbase, NC,
+                                  reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
         }
-        cl.sync();
+        __syncthreads();
+        if (P) ++nlarge, clarge += clock64() - tl0, mlarge += bs;
       }
     }
     if (P) {
@@ -518,7 +542,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       a.prof[2] = c3;
       a.prof[3] = nbat;
       a.prof[4] = nsimple;
-      a.prof[5] = a.prof[6] = 0;
+      a.prof[5] = nlarge;
+      a.prof[6] = clarge;
+      a.prof[8] = mlarge;
       a.prof[7] = CS;
     }
   }

@@ -24,7 +24,8 @@ for T in Ts:
     it = r.trace.iters[-1]
     print(f"T={T} CS={prof[7]} n={it.n} batches={nb} simple={prof[4]} order={it.order_ms:.3f} ms "
           f"({1e3 * it.order_ms / nb:.2f} us/batch) cycles/batch S1={prof[0] / nb:.0f} "
-          f"S2={prof[1] / nb:.0f} S3={prof[2] / nb:.0f}")
+          f"S2={prof[1] / nb:.0f} S3={prof[2] / nb:.0f}; batches beyond 32 members: {prof[5]} "
+          f"({prof[8]} members, {prof[6] / max(1, int(prof[5])):.0f} cycles each)")
     if os.environ.get("DG_STAMPS"):
         ng = max(1, nb - int(prof[4]))
         print("  general batches: cycles per batch (owner loop, CTA barrier, member wait, removal):",
