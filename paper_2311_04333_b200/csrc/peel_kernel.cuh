@@ -190,19 +190,21 @@ __device__ __forceinline__ void stamp(unsigned long long* prof, unsigned long lo
 
 // S3 over one member's row for warps [rank] of the nwj serving it: the row
 // [oj, oj + dj) as 16-byte quads indexed relative to its first quad; only the
-// first and last quad can be partial.
-template <class K, bool SMEM, bool ONE>
-__device__ __forceinline__ void remove_row(const uint4* adj4, K* keys, uint32_t keys_s,
-                                           uint64_t oj, uint32_t dj, uint32_t vj, uint32_t rank,
-                                           uint32_t nwj, uint32_t lane, uint32_t* cnt) {
-  const uint4* row = adj4 + (oj >> 2);
-  const uint32_t head = uint32_t(oj & 3), end = head + dj;  // valid elements [head, end)
-  const uint32_t nq = (end + 3) >> 2, stride = nwj * 32;
-  for (uint32_t b = rank * 32 + lane; b < nq; b += stride * UQ) {
-    uint4 x[UQ];
+// first and last quad can be partial.  A round = UQ quads per lane in flight.
+struct RowWalk {
+  const uint4* row;
+  uint32_t head, end, nq, stride;
+  __device__ __forceinline__ RowWalk(const uint4* adj4, uint64_t oj, uint32_t dj, uint32_t nwj)
+      : row(adj4 + (oj >> 2)), head(uint32_t(oj & 3)), end(uint32_t(oj & 3) + dj),
+        nq((uint32_t(oj & 3) + dj + 3) >> 2), stride(nwj * 32) {}
+  __device__ __forceinline__ void load(uint32_t b, uint4 (&x)[UQ]) const {
 #pragma unroll
     for (int k = 0; k < UQ; ++k)
       if (b + k * stride < nq) x[k] = __ldg(row + b + k * stride);
+  }
+  template <class K, bool SMEM, bool ONE>
+  __device__ __forceinline__ void proc(uint32_t b, const uint4 (&x)[UQ], K* keys,
+                                       uint32_t keys_s, uint32_t vj, uint32_t* cnt) const {
 #pragma unroll
     for (int k = 0; k < UQ; ++k) {
       const uint32_t t = b + k * stride;
@@ -217,6 +219,18 @@ __device__ __forceinline__ void remove_row(const uint4* adj4, K* keys, uint32_t 
           if (e0 + e >= head && e0 + e < end) dec_key<K, SMEM, ONE>(keys, keys_s, us[e], vj, cnt);
       }
     }
+  }
+};
+
+template <class K, bool SMEM, bool ONE>
+__device__ __forceinline__ void remove_row(const uint4* adj4, K* keys, uint32_t keys_s,
+                                           uint64_t oj, uint32_t dj, uint32_t vj, uint32_t rank,
+                                           uint32_t nwj, uint32_t lane, uint32_t* cnt) {
+  const RowWalk rw(adj4, oj, dj, nwj);
+  for (uint32_t b = rank * 32 + lane; b < rw.nq; b += rw.stride * UQ) {
+    uint4 x[UQ];
+    rw.load(b, x);
+    rw.proc<K, SMEM, ONE>(b, x, keys, keys_s, vj, cnt);
   }
 }
 
@@ -453,23 +467,41 @@ __global__ void __launch_bounds__(LB, 1) k_peel(Args<K> a) {
     const bool own = lane < NW && xw == gmin;
     const uint32_t ownmask = __ballot_sync(~0u, own);
     const uint32_t cc = own ? xc : 0u;
-    const uint32_t total = __reduce_add_sync(~0u, cc);
-    const uint32_t bs = a.one ? 1u : total;
-    PK_STAMP(2, uint32_t(gmin) + bs);
-    const bool mine = wm == gmin && lmin == gmin && lcnt;  // my chunk holds members
-    if (OFFS && (a.one || total == uint32_t(__popc(ownmask)))) {
-      // ---- simple batch: every owner warp holds exactly one member (or
-      // one-at-a-time), so the table names the whole batch in ascending id
-      // (owner warps ascend).  No staging, no barrier B.
-      ++nsimple;
-      const uint32_t xf = lane < NW ? s.wfirst[lane] : 0u;
+    // OFFS: assume a simple batch (one member per owner warp: bs = #owner
+    // warps) and issue the first round of the member's row loads now, so
+    // their L2 round trip overlaps the batch-size reduction and the check
+    const uint32_t npop = __popc(ownmask);
+    uint32_t xf = 0, j = 0, rank = 0, nwj = 0, lj = 0, vj = 0, oj = 0, dj = 0, b0 = 0;
+    uint4 x0[UQ];
+    if constexpr (OFFS) {
+      const uint32_t bss = a.one ? 1u : npop;
+      xf = lane < NW ? s.wfirst[lane] : 0u;
       const uint32_t xr0 = lane < NW ? s.wr0[lane] : 0u;
       const uint32_t xd = lane < NW ? s.wdeg[lane] : 0u;
       // owner lane L (table entry L) holds member rk(L) = #owner lanes below L
       const uint32_t rk = __popc(ownmask & ((1u << lane) - 1u));
-      const uint32_t wm3 = s.wmap[bs - 1][w];
-      const uint32_t j = wm3 & 0xffu, rank = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
-      const uint32_t lj = __ffs(__ballot_sync(~0u, own && rk == j)) - 1;  // my member's lane
+      if (bss == 1) {
+        j = 0, rank = w, nwj = NW;
+      } else {
+        const uint32_t wm3 = s.wmap[bss - 1][w];
+        j = wm3 & 0xffu, rank = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
+      }
+      lj = __ffs(__ballot_sync(~0u, own && rk == j)) - 1;  // my member's lane
+      vj = __shfl_sync(~0u, xf, lj);
+      oj = __shfl_sync(~0u, xr0, lj), dj = __shfl_sync(~0u, xd, lj);
+      b0 = rank * 32 + lane;
+      RowWalk(adj4, oj, dj, nwj).load(b0, x0);
+    }
+    const uint32_t total = __reduce_add_sync(~0u, cc);
+    const uint32_t bs = a.one ? 1u : total;
+    PK_STAMP(2, uint32_t(gmin) + bs);
+    const bool mine = wm == gmin && lmin == gmin && lcnt;  // my chunk holds members
+    if (OFFS && (a.one || total == npop)) {
+      // ---- simple batch: every owner warp holds exactly one member (or
+      // one-at-a-time), so the table names the whole batch in ascending id
+      // (owner warps ascend).  No staging, no barrier B.
+      ++nsimple;
+      const uint32_t rk = __popc(ownmask & ((1u << lane) - 1u));
       if (bs == 1) {
         if (w == NW - 1 && lane == lj) {
           a.perm[pos] = xf;
@@ -484,16 +516,25 @@ __global__ void __launch_bounds__(LB, 1) k_peel(Args<K> a) {
         __syncwarp();
         marked = mine;
       }
-      const uint32_t vj = __shfl_sync(~0u, xf, lj);
-      const uint32_t oj = __shfl_sync(~0u, xr0, lj), dj = __shfl_sync(~0u, xd, lj);
       uint32_t* cnt = s.cnt2[nbat & 1];
       PK_STAMP(3, 0);
       PK_STAMP(4, vj);
-      if (bs == 1)
-        remove_row<K, SMEM, true>(adj4, keys, keys_s, oj, dj, vj, rank, nwj, lane, nullptr);
-      else
-        remove_row<K, SMEM, false>(adj4, keys, keys_s, oj, dj, vj, rank, nwj, lane,
-                                       &cnt[j]);
+      const RowWalk rw(adj4, oj, dj, nwj);
+      if (bs == 1) {
+        rw.proc<K, SMEM, true>(b0, x0, keys, keys_s, vj, nullptr);
+        for (uint32_t b = b0 + rw.stride * UQ; b < rw.nq; b += rw.stride * UQ) {
+          uint4 x[UQ];
+          rw.load(b, x);
+          rw.proc<K, SMEM, true>(b, x, keys, keys_s, vj, nullptr);
+        }
+      } else {
+        rw.proc<K, SMEM, false>(b0, x0, keys, keys_s, vj, &cnt[j]);
+        for (uint32_t b = b0 + rw.stride * UQ; b < rw.nq; b += rw.stride * UQ) {
+          uint4 x[UQ];
+          rw.load(b, x);
+          rw.proc<K, SMEM, false>(b, x, keys, keys_s, vj, &cnt[j]);
+        }
+      }
       PK_STAMP(5, 0);
       __syncthreads();  // C
       pend_n = bs;
