@@ -182,10 +182,41 @@ def pinned_copy(a):
 
 
 # ------------------------------------------------------------------ reference arm
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_graph(cfg):
+    """The seeded graph as a host CSR, built on the CPU (no GPU code): RMAT by
+    the OpenMP builder og_par.c (checked equal to the oracle build and to the
+    device CSR), the others by the sequential oracle build."""
+    if cfg["kind"] == "rmat":
+        from oracle import rmat_graph_par
+        return rmat_graph_par(cfg["scale"], cfg["edge_factor"] << cfg["scale"], cfg["seed"])
+    from oracle import Oracle
+    u, v = host_pairs(cfg)
+    return Oracle().build(u, v)
+
+
 def run_reference(args, cfg, rank, world):
+    """The reference's own CPU implementation (oracle/_ref = the unmodified
+    densegraph library) on the same seeded graph, all host threads.
+
+    A STEP is one Greedy++ iteration of the reference's run() (framework.cpp:
+    105-153; IterRecord.ms = its ordering + Algorithm 3), the same unit our
+    arm sums: run() is called ceil((W+K)/T) times back to back, the first W
+    iterations are warm-up, the next K are timed; value = sum m_cur / sum
+    IterRecord.ms.  k-core edges/s = m / one timed exact_coreness."""
     if rank != 0:
         return 0
-    from oracle import Oracle, Reference, RunConfig, reference_available
+    from oracle import Reference, RunConfig, reference_available
     if not reference_available():
         print(json.dumps({"impl": "reference", "metric": METRIC,
                           "unavailable": "oracle/_ref/libdgref.so was not built (needs /root/reference at build time)"}))
@@ -193,33 +224,44 @@ def run_reference(args, cfg, rank, world):
     ref = Reference()
     threads = os.cpu_count() or 1
     ref.set_threads(threads)
-    u, v = host_pairs(cfg)
-    h = Oracle().build(u, v)
-    del u, v
+    t0 = time.perf_counter()
+    h = host_graph(cfg)
+    build_s = time.perf_counter() - t0
+    n, m = h.n, h.m
     rg = ref.from_csr(h)
-    rcfg = RunConfig(iterations=cfg["T"], epsilon=cfg["eps"])
-    for _ in range(args.warmup):
-        ref.run(rg, rcfg, threads=threads)
-    edges = ms_it = 0.0
-    t_steps = []
-    for _ in range(args.steps):
+    del h
+    t0 = time.perf_counter()
+    ref.coreness(rg)
+    kc_s = time.perf_counter() - t0
+    T = cfg["T"]
+    need = args.warmup + args.steps
+    rcfg = RunConfig(iterations=T, epsilon=cfg["eps"])
+    its, run_ms, last = [], [], None
+    while len(its) < need:
         t0 = time.perf_counter()
-        r = ref.run(rg, rcfg, threads=threads)
-        t_steps.append((time.perf_counter() - t0) * 1e3)
-        edges += sum(t[4] for t in r.trace)
-        ms_it += sum(r.iter_ms)
-    value = edges / (ms_it / 1e3)
+        last = ref.run(rg, rcfg, threads=threads)
+        run_ms.append((time.perf_counter() - t0) * 1e3)
+        its += [(t[4], ms) for t, ms in zip(last.trace, last.iter_ms)]
+    timed = its[args.warmup:need]
+    edges = sum(e for e, _ in timed)
+    ms = sum(x for _, x in timed)
+    value = edges / (ms / 1e3)
+    sample = (f"{args.steps} timed Greedy++ iterations (after {args.warmup} warm-up) of "
+              f"{len(run_ms)} back-to-back reference run()s (T={T}), value = sum m_cur / "
+              f"sum IterRecord.ms; k-core = one exact_coreness")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sum(t_steps) / len(t_steps), "higher_is_better": True,
+        "ms_per_step": ms / len(timed), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": workload_config(args.config, cfg, h.n, h.m, world),
+        "config": workload_config(args.config, cfg, n, m, world),
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} full reference run()s (k-core + prune + T={cfg['T']} Greedy++) of the same graph; value = sum m_cur / sum IterRecord.ms"},
+                         "cpu": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "reference_detail": {"init_ms": r.times[1], "coreness_ms_incl_get_core": r.times[0],
-                             "total_ms": r.times[2], "iter_ms": r.iter_ms[:len(r.trace)]},
+        "kcore": {"value": m / kc_s, "unit": "edges/s", "ms": kc_s * 1e3},
+        "reference_detail": {"host_build_s": round(build_s, 2), "run_ms": run_ms,
+                             "init_ms": last.times[1], "coreness_ms_incl_get_core": last.times[0],
+                             "iter_ms": [round(x, 2) for _, x in its]},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -268,11 +310,15 @@ def run_ours(args, cfg, rank, world, local):
     clk = clocks.summary(t_start, t_end)
     clocks.stop()
 
-    edges = sum(it.m for r in res for it in r.trace.iters)
-    it_ms = sum(it.ms for r in res for it in r.trace.iters)
-    order_ms = sum(it.order_ms for r in res for it in r.trace.iters)
-    batches = sum(it.batches for r in res for it in r.trace.iters)
-    peel_bytes = sum(8 * (it.n + 1) + 8 * it.m + 16 * it.n for r in res for it in r.trace.iters)
+    iters = [it for r in res for it in r.trace.iters]
+    edges = sum(it.m for it in iters)
+    it_ms = sum(it.ms for it in iters)          # t_iter = ordering + Alg. 3 (CUDA events)
+    order_ms = sum(it.order_ms for it in iters)
+    batches = sum(it.batches for it in iters)
+    # B_it = 8(n+1) offs + 8m adj + 16n loads r+w + 4n perm = 8m + 28n + 8
+    it_bytes = sum(8 * (it.n + 1) + 8 * it.m + 16 * it.n + 4 * it.n for it in iters)
+    # the peel kernel alone: offs + adj + loads read + perm + raw charges written
+    peel_bytes = sum(8 * (it.n + 1) + 8 * it.m + 8 * it.n + 4 * it.n + 8 * it.n for it in iters)
     kc_ms = sum(r.trace.init.coreness_kernel_ms for r in res)
     dev_ms = sum(r.device_ms for r in res)
     # max over ranks for times, sum for work
@@ -281,9 +327,15 @@ def run_ours(args, cfg, rank, world, local):
     edges_all, kc_edges_all = allreduce([float(edges), float(m * args.steps)], "sum", world, local)
     value = edges_all / (it_ms_max / 1e3)
     kcore_value = kc_edges_all / (kc_ms_max / 1e3)
+    it_achieved = it_bytes / (it_ms / 1e3) / 1e9
     peel_achieved = peel_bytes / (order_ms / 1e3) / 1e9
+    # B_kc = 8(n+1) offs + 8m adj + 4n degree init + 4n labels; the timed
+    # region holds the degree-init kernel, the bitmap fill and the k-core kernel
     kc_bytes = 8 * m + 16 * n + 8
     kc_achieved = kc_bytes * args.steps / (kc_ms / 1e3) / 1e9
+    big = max(iters, key=lambda it: it.n * 1.0 * it.ms)
+    peel_kernel = "k_peel_cluster" if big.n > 16384 else "k_peel"
+    tr = traffic()
 
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
@@ -296,20 +348,27 @@ def run_ours(args, cfg, rank, world, local):
                   "roofline": {"bound": "hbm", "achieved": kc_achieved, "peak": hbm,
                                "unit": "GB/s", "frac": kc_achieved / hbm,
                                "algorithmic_bytes": kc_bytes, "peak_kind": peak_kind,
-                               "traffic": traffic().get("k_coreness", {}).get(
+                               "kernel": "k_coreness (+ k_init_deg, bitmap fill)",
+                               "traffic": tr.get(f"k_coreness_{args.config}", {}).get(
                                    "dram_bytes_per_launch")}},
-        "roofline": {"bound": "hbm", "achieved": peel_achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": peel_achieved / hbm,
-                     "traffic": traffic().get("k_peel", {}).get("dram_bytes_per_launch"),
-                     "traffic_note": traffic().get("k_peel", {}).get("launch"),
-                     "kernel": "k_peel (Greedy++ batch peel, fused Alg.3 charges)",
-                     "bytes_per_launch": "8(n+1) offs + 8m adj + 8n loads + 4n perm + 4n charges",
+        "roofline": {"bound": "hbm", "achieved": it_achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": it_achieved / hbm,
+                     "traffic": tr.get(f"{peel_kernel}_{args.config}", {}).get("dram_bytes_per_launch"),
+                     "traffic_note": tr.get(f"{peel_kernel}_{args.config}", {}).get("launch"),
+                     "kernel": f"Greedy++ iteration: {peel_kernel} (batch peel, fused Alg.3 charges) + k_alg3",
+                     "bytes_per_iteration": "8(n+1) offs + 8m adj + 16n loads r+w + 4n perm (SURVEY 8d)",
+                     "time": "t_iter = CUDA events around ordering + Alg. 3, summed over the timed iterations",
+                     "peel_kernel_only": {"achieved": peel_achieved, "frac": peel_achieved / hbm,
+                                          "bytes": "8(n+1) + 8m + 8n loads + 4n perm + 8n raw charges",
+                                          "time": "ordering events only"},
                      "peak_kind": peak_kind},
-        "greedy": {"iterations": sum(len(r.trace.iters) for r in res),
-                   "batches_per_iter": batches / max(1, sum(len(r.trace.iters) for r in res)),
+        "greedy": {"iterations": len(iters),
+                   "batches_per_iter": batches / max(1, len(iters)),
                    "us_per_batch": order_ms * 1e3 / max(1, batches),
-                   "order_ms_per_iter": order_ms / max(1, sum(len(r.trace.iters) for r in res)),
-                   "update_ms_per_iter": (it_ms - order_ms) / max(1, sum(len(r.trace.iters) for r in res)),
+                   "order_ms_per_iter": order_ms / max(1, len(iters)),
+                   "update_ms_per_iter": (it_ms - order_ms) / max(1, len(iters)),
+                   "per_iteration": [[it.n, it.m, it.batches, round(it.ms, 3)]
+                                     for it in res[0].trace.iters],
                    "core_n_m": [res[0].trace.init.pruned_n, res[0].trace.init.pruned_m],
                    "reprunes": res[0].reprunes,
                    "best": [res[0].best.edges, res[0].best.verts],
@@ -368,7 +427,7 @@ def cpu_baseline(cfg, offs, adj, orig):
     from oracle import HostGraph, Reference, RunConfig, reference_available
     if not reference_available():
         return {"value": None, "unit": "edges/s", "cores": 0, "kind": "reference",
-                "sample": "unavailable: oracle/_ref not built"}
+                "cpu": cpu_model(), "sample": "unavailable: oracle/_ref not built"}
     ref = Reference()
     threads = os.cpu_count() or 1
     ref.set_threads(threads)
@@ -380,7 +439,7 @@ def cpu_baseline(cfg, offs, adj, orig):
     r = ref.run(rg, RunConfig(iterations=cfg["T"], epsilon=cfg["eps"]), threads=threads)
     edges = sum(t[4] for t in r.trace)
     return {"value": edges / (sum(r.iter_ms) / 1e3), "unit": "edges/s", "cores": threads,
-            "kind": "reference",
+            "kind": "reference", "cpu": cpu_model(),
             "sample": f"one full reference run() (T={cfg['T']}) + one exact_coreness on the same graph",
             "kcore_value": m / kc_s, "run_total_ms": r.times[2], "init_ms": r.times[1]}
 
@@ -391,7 +450,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="rmat22", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="rmat26", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <memory>
 #include <span>
+#include <mutex>
 #include <vector>
 
 #include "dg_b200.h"
@@ -66,14 +67,24 @@ struct Graph {
   Density density() const { return {m, n == 0 ? 1 : n}; }
 
   // ---- B200 device cache (not part of the reference layout) ----
+  // The reference's Graph is immutable after construction and safe to share
+  // read-only: the cache is keyed on the sizes and storage of
+  // offs/adj/orig (a caller that edits those fields in place after the first
+  // device call must assign a fresh Graph), and the lazy upload is serialised
+  // so concurrent readers of one Graph never race on it.
   dg_graph* device() const {
-    if (!dev_ || dev_n_ != n || dev_adj_ != adj.data()) {
+    std::lock_guard<std::mutex> lk(device_mutex());
+    if (!dev_ || dev_n_ != n || dev_adj_ != adj.data() || dev_offs_ != offs.data() ||
+        dev_orig_ != orig.data() || dev_arcs_ != adj.size()) {
       dg_graph* h = nullptr;
       detail::check(dg_graph_from_csr(n, offs.empty() ? zero_offs() : offs.data(), adj.data(),
                                       orig.data(), 0, &h));
       dev_ = detail::Handle(h, detail::HandleDeleter{});
       dev_n_ = n;
       dev_adj_ = adj.data();
+      dev_offs_ = offs.data();
+      dev_orig_ = orig.data();
+      dev_arcs_ = adj.size();
     }
     return dev_.get();
   }
@@ -91,6 +102,9 @@ struct Graph {
     g.dev_ = std::move(hold);
     g.dev_n_ = dn;
     g.dev_adj_ = g.adj.data();
+    g.dev_offs_ = g.offs.data();
+    g.dev_orig_ = g.orig.data();
+    g.dev_arcs_ = g.adj.size();
     return g;
   }
 
@@ -99,9 +113,16 @@ struct Graph {
     static const u64 z = 0;
     return &z;
   }
+  static std::mutex& device_mutex() {
+    static std::mutex mu;
+    return mu;
+  }
   mutable detail::Handle dev_;
   mutable u64 dev_n_ = 0;
   mutable const u32* dev_adj_ = nullptr;
+  mutable const u64* dev_offs_ = nullptr;
+  mutable const u64* dev_orig_ = nullptr;
+  mutable std::size_t dev_arcs_ = 0;
 };
 
 // Subgraph induced by keep[v] != 0 (graph.hpp:47-80); new ids follow the

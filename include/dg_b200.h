@@ -275,6 +275,9 @@ dg_status dg_synchronize(void);
 dg_status dg_set_device(int device);
 /* Number of this library's own kernels launched so far in this process. */
 uint64_t dg_launch_count(void);
+/* Return every cached block of the library's private device memory pool to
+ * the driver (the pool keeps up to 16 GiB of freed scratch between calls). */
+dg_status dg_trim_memory(void);
 /* Evict L2 by writing a 256 MiB scratch buffer (bench hygiene between steps). */
 dg_status dg_flush_l2(void);
 

@@ -23,6 +23,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libdgref.so")
+PAR_SO = os.path.join(HERE, "liboracle_par.so")
 
 u64p = C.POINTER(C.c_uint64)
 u32p = C.POINTER(C.c_uint32)
@@ -297,6 +298,22 @@ class Oracle:
         v = np.zeros(pairs, np.uint64)
         self.lib.og_gen_chung_lu(n, pairs, chung_lu_root(n), seed, _p(u, u64p), _p(v, u64p))
         return u, v
+
+
+def rmat_graph_par(scale: int, samples: int, seed: int, threads: int = 0) -> HostGraph:
+    """Seeded RMAT graph built on the host with OpenMP (og_par.c): the CSR of
+    ``Oracle().build(*Oracle().gen_rmat(scale, samples, seed))``, fast enough
+    for RMAT-26.  Input preparation for the reference arm only."""
+    if not os.path.exists(PAR_SO):
+        raise FileNotFoundError(f"{PAR_SO} missing: run `make -C oracle`")
+    lib = C.CDLL(PAR_SO)
+    lib.ogp_rmat_graph.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
+                                   C.POINTER(OgGraph)]
+    og = OgGraph()
+    st = lib.ogp_rmat_graph(scale, samples, seed, threads, C.byref(og))
+    if st:
+        raise OracleError(st, "ogp_rmat_graph failed")
+    return _from_og(lib, og)
 
 
 def chung_lu_root(n: int) -> float:

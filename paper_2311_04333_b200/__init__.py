@@ -543,6 +543,11 @@ def flush_l2() -> None:
     _chk(LIB.dg_flush_l2())
 
 
+def trim_memory() -> None:
+    """Return the library's cached device memory to the driver (dg_trim_memory)."""
+    _chk(LIB.dg_trim_memory())
+
+
 def synchronize() -> None:
     _chk(LIB.dg_synchronize())
 

@@ -105,6 +105,7 @@ PROTOTYPES = {
     "dg_set_device": (C.c_int, [C.c_int]),
     "dg_launch_count": (C.c_uint64, []),
     "dg_flush_l2": (C.c_int, []),
+    "dg_trim_memory": (C.c_int, []),
     "dg_microbench": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_double)]),
     "dg_peel_profile": (C.c_int, [u64p]),
     "dg_peel_trace_arm": (C.c_int, [C.c_uint32]),

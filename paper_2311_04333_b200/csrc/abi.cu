@@ -18,6 +18,8 @@ namespace dgb {
 namespace {
 constexpr int kMaxDev = 64;
 cudaStream_t g_streams[kMaxDev] = {};
+cudaMemPool_t g_pools[kMaxDev] = {};
+constexpr uint64_t kPoolKeep = 16ULL << 30;
 int g_sms[kMaxDev] = {};
 std::mutex g_mu;
 thread_local std::string g_err;
@@ -44,14 +46,32 @@ cudaStream_t stream() {
         throw DgError(DG_E_CUDA, "this library is built for sm_100a (B200); device is sm_" +
                                      std::to_string(p.major) + std::to_string(p.minor));
       g_sms[d] = p.multiProcessorCount;
-      cudaMemPool_t pool;
-      DG_CUDA(cudaDeviceGetDefaultMemPool(&pool, d));
-      uint64_t thr = ~0ULL;  // keep freed blocks cached in the pool
-      DG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      // A PRIVATE stream-ordered pool: the device's default pool (which torch,
+      // NCCL and other users of cudaMallocAsync share) keeps its settings.
+      // Freed blocks stay cached up to kPoolKeep bytes (a run's scratch is
+      // reused by the next run); beyond that the pool returns memory to the
+      // driver at the next synchronisation, and dg_trim_memory releases all.
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = d;
+      DG_CUDA(cudaMemPoolCreate(&g_pools[d], &props));
+      uint64_t thr = std::min<uint64_t>(kPoolKeep, p.totalGlobalMem / 8);
+      DG_CUDA(cudaMemPoolSetAttribute(g_pools[d], cudaMemPoolAttrReleaseThreshold, &thr));
       DG_CUDA(cudaStreamCreateWithFlags(&g_streams[d], cudaStreamNonBlocking));
     }
   }
   return g_streams[d];
+}
+
+cudaMemPool_t mem_pool() {
+  stream();
+  return g_pools[cur_dev()];
+}
+
+void trim_memory() {
+  stream_sync();
+  DG_CUDA(cudaMemPoolTrimTo(mem_pool(), 0));
 }
 
 int num_sms() {
@@ -65,6 +85,7 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void set_last_error(const char* what) { g_err = what; }
 
 namespace {
 
@@ -409,23 +430,6 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
 
 // ==================================================================== C ABI
 using namespace dgb;
-
-#define DG_API_BEGIN try {
-#define DG_API_END                          \
-  return DG_OK;                             \
-  }                                         \
-  catch (const DgError& e) {                \
-    g_err = e.what();                       \
-    return e.code;                          \
-  }                                         \
-  catch (const std::bad_alloc& e) {         \
-    g_err = "host allocation failed";       \
-    return DG_E_NOMEM;                      \
-  }                                         \
-  catch (const std::exception& e) {         \
-    g_err = e.what();                       \
-    return DG_E_INVARIANT;                  \
-  }
 
 namespace {
 // Upload a host array (or copy a device array) into a fresh device buffer.
@@ -806,6 +810,12 @@ dg_status dg_set_device(int device) {
 }
 
 uint64_t dg_launch_count(void) { return g_launches.load(); }
+
+dg_status dg_trim_memory(void) {
+  DG_API_BEGIN
+  trim_memory();
+  DG_API_END
+}
 
 dg_status dg_flush_l2(void) {
   DG_API_BEGIN

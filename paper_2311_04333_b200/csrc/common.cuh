@@ -8,6 +8,8 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -38,6 +40,27 @@ struct DgError : std::runtime_error {
   } while (0)
 
 void count_launch();
+void set_last_error(const char* what);  // the thread's dg_last_error() text
+
+// Every extern "C" entry point: exceptions never cross the ABI; the status
+// code maps onto the reference's exception type and dg_last_error() holds
+// the message.
+#define DG_API_BEGIN try {
+#define DG_API_END                                  \
+  return DG_OK;                                     \
+  }                                                 \
+  catch (const ::dgb::DgError& e) {                 \
+    ::dgb::set_last_error(e.what());                \
+    return e.code;                                  \
+  }                                                 \
+  catch (const std::bad_alloc&) {                   \
+    ::dgb::set_last_error("host allocation failed"); \
+    return DG_E_NOMEM;                              \
+  }                                                 \
+  catch (const std::exception& e) {                 \
+    ::dgb::set_last_error(e.what());                \
+    return DG_E_INVARIANT;                          \
+  }
 #define DG_CHECK_LAUNCH()            \
   do {                               \
     DG_CUDA(cudaGetLastError());     \
@@ -48,10 +71,12 @@ void count_launch();
 // lazily).  Every entry point enqueues on it and synchronises before
 // returning, so calls are externally synchronous like the reference's.
 cudaStream_t stream();
+cudaMemPool_t mem_pool();  // the library's private stream-ordered pool
+void trim_memory();        // release every cached block of mem_pool()
 int num_sms();
 void stream_sync();
 
-// Stream-ordered device buffer (cudaMallocAsync on the library stream).
+// Stream-ordered device buffer (the library's private pool, library stream).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -76,7 +101,8 @@ struct DevBuf {
     // +16 bytes of slack: kernels may read a whole 16-byte vector that
     // straddles the end of an array (e.g. the last adjacency quad)
     if (count)
-      DG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T) + 16, stream()));
+      DG_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), count * sizeof(T) + 16,
+                                      mem_pool(), stream()));
   }
   void release() {
     if (p) cudaFreeAsync(p, stream());
@@ -218,8 +244,16 @@ struct GridBarrier {
   uint32_t count;
   uint32_t gen;
   uint32_t abort;
-  uint32_t pad;
+  uint32_t timeout_s;  // give up after ~timeout_s seconds of spinning (0: 60)
 };
+
+// Host side: the spin limit of grid barriers, DG_BARRIER_TIMEOUT_S (default
+// 60 s; a debugger or compute-sanitizer may need more).
+inline uint32_t barrier_timeout_s() {
+  const char* e = getenv("DG_BARRIER_TIMEOUT_S");
+  const long v = e ? atol(e) : 0;
+  return v > 0 ? uint32_t(v) : 60u;
+}
 
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
@@ -256,7 +290,8 @@ __device__ __forceinline__ bool grid_sync(GridBarrier* b, uint32_t nblocks, uint
     while (((old ^ ld_acquire_u32(&b->count)) & 0x80000000u) == 0) {
       if ((++spins & 1023u) == 0) {
         if (ld_relaxed_u32(&b->abort)) break;
-        if (clock64() - t0 > (1LL << 33)) {  // ~4 s at 2 GHz: give up, do not hang
+        const long long lim = (long long)(b->timeout_s ? b->timeout_s : 60u) << 31;
+        if (clock64() - t0 > lim) {  // ~timeout_s seconds at 2 GHz: give up, do not hang
           atomicExch(&b->abort, 1u);
           break;
         }

@@ -555,7 +555,7 @@ __global__ void k_init_deg(const uint64_t* offs, uint64_t n, uint32_t* deg, uint
   }
 }
 
-__global__ void k_init_acc(Acc* acc, GridBarrier* bar) {
+__global__ void k_init_acc(Acc* acc, GridBarrier* bar, uint32_t timeout_s) {
   if (threadIdx.x < 3) {
     acc[threadIdx.x].front = 0;
     acc[threadIdx.x].live = 0;
@@ -564,7 +564,7 @@ __global__ void k_init_acc(Acc* acc, GridBarrier* bar) {
     acc[threadIdx.x].live2 = 0;
     acc[threadIdx.x].ccnt = 0;
   }
-  if (threadIdx.x == 0) *bar = GridBarrier{0, 0, 0, 0};
+  if (threadIdx.x == 0) *bar = GridBarrier{0, 0, 0, timeout_s};
 }
 
 }  // namespace
@@ -600,10 +600,7 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   bool bm = true;
   if (const char* e = getenv("DG_KCORE_BITMAP")) bm = e[0] == '1';
   DevBuf<uint32_t> alive;
-  if (bm) {
-    alive.alloc((n + 31) / 32);
-    DG_CUDA(cudaMemsetAsync(alive.get(), 0xff, ((n + 31) / 32) * 4, stream()));
-  }
+  if (bm) alive.alloc((n + 31) / 32);
   DevBuf<uint64_t> fa0(n), fa1(n), fo0(n), fo1(n);
   const uint64_t nch = (2 * g.m) / CH + 2;
   DevBuf<uint32_t> cse0(nch), cse1(nch);
@@ -611,9 +608,16 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   DevBuf<GridBarrier> bar(1);
   DevBuf<uint32_t> out(3);
   out.zero();
+  // the timed region (CoreOut::kernel_ms) holds every pass over the graph:
+  // bitmap fill, degree init (the 4n + 8n of B_kc) and the peel kernel
+  cudaEvent_t e0, e1;
+  DG_CUDA(cudaEventCreate(&e0));
+  DG_CUDA(cudaEventCreate(&e1));
+  DG_CUDA(cudaEventRecord(e0, stream()));
+  if (bm) DG_CUDA(cudaMemsetAsync(alive.get(), 0xff, ((n + 31) / 32) * 4, stream()));
   k_init_deg<<<grid_for(n, 256), 256, 0, stream()>>>(g.offs.get(), n, deg.get(), d_labels);
   DG_CHECK_LAUNCH();
-  k_init_acc<<<1, 32, 0, stream()>>>(acc.get(), bar.get());
+  k_init_acc<<<1, 32, 0, stream()>>>(acc.get(), bar.get(), barrier_timeout_s());
   DG_CHECK_LAUNCH();
 
   const size_t smem = sizeof(Smem);
@@ -644,10 +648,6 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
               c_num,
               c_den};
   void* params[] = {&args};
-  cudaEvent_t e0, e1;
-  DG_CUDA(cudaEventCreate(&e0));
-  DG_CUDA(cudaEventCreate(&e1));
-  DG_CUDA(cudaEventRecord(e0, stream()));
   DG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(blocks), dim3(KC_THREADS), params,
                                       smem, stream()));
   count_launch();
@@ -659,6 +659,10 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   DG_CUDA(cudaEventElapsedTime(&r.kernel_ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (h[2] == 4)
+    throw DgError(DG_E_INVARIANT,
+                  "coreness kernel: grid barrier timeout (a CTA did not arrive within "
+                  "DG_BARRIER_TIMEOUT_S seconds)");
   if (h[2]) {
     char buf[128];
     snprintf(buf, sizeof buf, "coreness kernel failed internal check (code %u)", h[2]);

@@ -267,11 +267,3 @@ extern "C" dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]) {
   }
 }
 
-namespace dgb {
-extern int g_peel_mode;
-}
-extern "C" dg_status dg_set_peel_mode(int mode) {
-  if (mode < 0 || mode > 3) return DG_E_PARAM;
-  dgb::g_peel_mode = mode;
-  return DG_OK;
-}

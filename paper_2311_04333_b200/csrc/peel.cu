@@ -16,6 +16,8 @@
 // pre-update loads, and the next iteration's key range -- one CTA.
 #include <cub/cub.cuh>
 
+#include <atomic>
+
 #include "internal.cuh"
 #include "peel_kernel.cuh"
 #include "peel_cluster.cuh"
@@ -31,7 +33,7 @@ constexpr size_t kSmemCap = 227 * 1024;
 }  // namespace
 
 constexpr uint64_t kQueueMinN = 16384;
-int g_peel_mode = 0;  // dg_set_peel_mode: 0 auto, 1 scanning single-CTA kernel, 2 cluster, 3 candidate list
+std::atomic<int> g_peel_mode{0};  // dg_set_peel_mode: 0 auto, 1 scanning single-CTA kernel, 2 cluster, 3 candidate list
 
 namespace {
 
@@ -503,16 +505,17 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
   // batch mode beyond kQueueMinN: the cluster kernel (RMAT-22's 35K core
   // 3.52 vs 4.22 us per batch for the candidate-list kernel, RMAT-26's 17.9K
   // core 2.98 vs 3.20), the candidate-list kernel when no cluster fits
-  if (k32 && !one_at_a_time && g_peel_mode == 0 && g.n > kQueueMinN) {
+  const int mode = g_peel_mode.load(std::memory_order_relaxed);
+  if (k32 && !one_at_a_time && mode == 0 && g.n > kQueueMinN) {
     if (launch_cluster<16>(g, d_loads, base, false, d_perm, d_raw, d_batches)) return;
     if (launch_cluster<8>(g, d_loads, base, false, d_perm, d_raw, d_batches)) return;
   }
   if (k32 && !one_at_a_time &&
-      ((g_peel_mode == 0 && g.n > kQueueMinN) || g_peel_mode == 3)) {
+      ((mode == 0 && g.n > kQueueMinN) || mode == 3)) {
     if (offs32 && launch_queue<true>(g, d_loads, base, vq, d_perm, d_raw, d_batches)) return;
     if (launch_queue<false>(g, d_loads, base, vq, d_perm, d_raw, d_batches)) return;
   }
-  if (k32 && g_peel_mode == 2) {
+  if (k32 && mode == 2) {
     if (launch_cluster<16>(g, d_loads, base, one_at_a_time, d_perm, d_raw, d_batches)) return;
     if (launch_cluster<8>(g, d_loads, base, one_at_a_time, d_perm, d_raw, d_batches)) return;
   }
@@ -523,7 +526,7 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
     if (peelk::smem_bytes<uint32_t, false>(4 * vq, true) <= kSmemCap &&
         launch_vec<false>(g, d_loads, base, one_at_a_time, vq, d_perm, d_raw, d_batches))
       return;
-    if (g_peel_mode != 1) {
+    if (mode != 1) {
       if (launch_cluster<16>(g, d_loads, base, one_at_a_time, d_perm, d_raw, d_batches)) return;
       if (launch_cluster<8>(g, d_loads, base, one_at_a_time, d_perm, d_raw, d_batches)) return;
     }
@@ -642,3 +645,9 @@ void alg3(const dg_graph& g, const uint32_t* d_perm, const uint32_t* d_charges,
 }
 
 }  // namespace dgb
+
+extern "C" dg_status dg_set_peel_mode(int mode) {
+  if (mode < 0 || mode > 3) return DG_E_PARAM;
+  dgb::g_peel_mode.store(mode, std::memory_order_relaxed);
+  return DG_OK;
+}

@@ -190,17 +190,6 @@ __global__ void k_sh_expand_peer(const uint64_t* offs, const uint32_t* adj, cons
 
 using namespace dgb;
 
-#define SH_TRY try {
-#define SH_END                  \
-  return DG_OK;                 \
-  }                             \
-  catch (const DgError& e) {    \
-    return e.code;              \
-  }                             \
-  catch (...) {                 \
-    return DG_E_INVARIANT;      \
-  }
-
 extern "C" {
 
 // common tail: state arrays, degree init
@@ -244,7 +233,7 @@ static void shard_check(uint64_t n, const uint64_t* bounds, uint32_t P, uint32_t
 
 dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P, uint32_t rank,
                           dg_shard** out) {
-  SH_TRY
+  DG_API_BEGIN
   if (!g || !out) throw DgError(DG_E_PARAM, "bad shard arguments");
   shard_check(g->n, bounds, P, rank);
   auto s = std::make_unique<dg_shard>();
@@ -269,13 +258,13 @@ dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P,
   shard_init_state(s.get(), bounds, P);
   s->peers[rank] = s->own;
   *out = s.release();
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_create_rows(uint64_t n, const uint64_t* bounds, uint32_t P, uint32_t rank,
                                const uint64_t* offs, const uint32_t* adj, int on_device,
                                dg_shard** out) {
-  SH_TRY
+  DG_API_BEGIN
   if (!out || !offs) throw DgError(DG_E_PARAM, "bad shard arguments");
   shard_check(n, bounds, P, rank);
   auto s = std::make_unique<dg_shard>();
@@ -310,7 +299,7 @@ dg_status dg_shard_create_rows(uint64_t n, const uint64_t* bounds, uint32_t P, u
   shard_init_state(s.get(), bounds, P);
   s->peers[rank] = s->own;
   *out = s.release();
-  SH_END
+  DG_API_END
 }
 
 void dg_shard_free(dg_shard* s) {
@@ -321,7 +310,7 @@ void dg_shard_free(dg_shard* s) {
 }
 
 dg_status dg_shard_min_alive(dg_shard* s, uint32_t* out) {
-  SH_TRY
+  DG_API_BEGIN
   const uint64_t nl = s->hi - s->lo;
   unsigned long long init = kUnset;
   h2d(s->cnt.get() + 1, &init, 1);
@@ -331,11 +320,11 @@ dg_status dg_shard_min_alive(dg_shard* s, uint32_t* out) {
     DG_CHECK_LAUNCH();
   }
   *out = uint32_t(read_scalar(s->cnt.get() + 1));
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_collect(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* nfront) {
-  SH_TRY
+  DG_API_BEGIN
   const uint64_t nl = s->hi - s->lo;
   s->cnt.zero();
   if (nl) {
@@ -346,11 +335,11 @@ dg_status dg_shard_collect(dg_shard* s, uint32_t bound, uint32_t label, uint64_t
   }
   s->nfront = read_scalar(s->cnt.get());
   *nfront = s->nfront;
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_count_remote(dg_shard* s, uint64_t* counts) {
-  SH_TRY
+  DG_API_BEGIN
   s->cnt.zero();
   if (s->nfront) {
     k_sh_expand<false><<<grid_for(s->nfront * 32, 256), 256, 0, stream()>>>(
@@ -363,12 +352,12 @@ dg_status dg_shard_count_remote(dg_shard* s, uint64_t* counts) {
   d2h(h.data(), s->cnt.get() + 2, s->P);
   stream_sync();
   for (uint32_t r = 0; r < s->P; ++r) counts[r] = h[r];
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_expand(dg_shard* s, uint32_t bound, uint32_t label, const uint64_t* displs,
                           uint32_t* d_send) {
-  SH_TRY
+  DG_API_BEGIN
   DevBuf<unsigned long long> cur(s->P);
   std::vector<unsigned long long> h(displs, displs + s->P);
   h2d(cur.get(), h.data(), s->P);
@@ -381,12 +370,12 @@ dg_status dg_shard_expand(dg_shard* s, uint32_t bound, uint32_t label, const uin
     DG_CHECK_LAUNCH();
   }
   stream_sync();
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_apply(dg_shard* s, const uint32_t* d_recv, uint64_t nrecv, uint32_t bound,
                          uint32_t label, uint64_t* nnext) {
-  SH_TRY
+  DG_API_BEGIN
   if (nrecv) {
     k_sh_apply<<<grid_for(nrecv, 256), 256, 0, stream()>>>(d_recv, nrecv, s->lo, s->own.deg,
                                                            s->own.labels, bound, label,
@@ -396,7 +385,7 @@ dg_status dg_shard_apply(dg_shard* s, const uint32_t* d_recv, uint64_t nrecv, ui
   s->nfront = read_scalar(s->cnt.get());
   s->cur ^= 1;
   *nnext = s->nfront;
-  SH_END
+  DG_API_END
 }
 
 // ---- peer mode
@@ -410,17 +399,17 @@ static void peer_set(dg_shard* s, uint32_t rank, void* block) {
 }
 
 dg_status dg_shard_ipc_handle(const dg_shard* s, void* handle) {
-  SH_TRY
+  DG_API_BEGIN
   if (!s || !handle) throw DgError(DG_E_PARAM, "null argument");
   cudaIpcMemHandle_t h;
   DG_CUDA(cudaIpcGetMemHandle(&h, s->block));
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
   memcpy(handle, &h, sizeof h);
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_peer_open(dg_shard* s, uint32_t rank, const void* handle) {
-  SH_TRY
+  DG_API_BEGIN
   if (!s || !handle) throw DgError(DG_E_PARAM, "null argument");
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, sizeof h);
@@ -428,19 +417,19 @@ dg_status dg_shard_peer_open(dg_shard* s, uint32_t rank, const void* handle) {
   DG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
   s->opened.push_back(p);
   peer_set(s, rank, p);
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_peer_link(dg_shard* s, uint32_t rank, const dg_shard* other) {
-  SH_TRY
+  DG_API_BEGIN
   if (!s || !other) throw DgError(DG_E_PARAM, "null argument");
   if (other->P != s->P || other->n != s->n) throw DgError(DG_E_PARAM, "shards of different graphs");
   peer_set(s, rank, other->block);
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_expand_peer(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* produced) {
-  SH_TRY
+  DG_API_BEGIN
   if (!s || !produced) throw DgError(DG_E_PARAM, "null argument");
   if (s->P > kMaxPeers) throw DgError(DG_E_PARAM, "peer mode supports at most 64 shards");
   if (!s->peers_ready) {
@@ -461,23 +450,23 @@ dg_status dg_shard_expand_peer(dg_shard* s, uint32_t bound, uint32_t label, uint
     DG_CHECK_LAUNCH();
   }
   *produced = read_scalar(s->cnt.get());
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_finish_round(dg_shard* s, uint64_t* nnext) {
-  SH_TRY
+  DG_API_BEGIN
   if (!s || !nnext) throw DgError(DG_E_PARAM, "null argument");
   s->nfront = read_scalar(s->own.ctr + (s->cur ^ 1));
   s->cur ^= 1;
   *nnext = s->nfront;
-  SH_END
+  DG_API_END
 }
 
 dg_status dg_shard_labels(const dg_shard* s, uint32_t* labels) {
-  SH_TRY
+  DG_API_BEGIN
   d2h(labels, s->own.labels, s->hi - s->lo);
   stream_sync();
-  SH_END
+  DG_API_END
 }
 
 }  // extern "C"

@@ -29,6 +29,8 @@ CudaShard.from_rows (dg_shard_create_rows, device pointers).
 """
 from __future__ import annotations
 
+import os
+
 from typing import List, Sequence
 
 import numpy as np
@@ -236,18 +238,40 @@ def prune_distributed(pairs, comm, make_shard, cfg, peer: bool = False):
     return offs, adj, orig, lab, kmax, rounds
 
 
-def run_distributed(u, v, cfg=None):
+def peer_capable() -> bool:
+    """Every rank of the job on this node, and this GPU can map every other
+    local GPU's memory (CUDA IPC over NVLink): the fused peer-memory exchange
+    applies.  Otherwise (multi-node jobs, no P2P) the NCCL all-to-all rounds."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size()
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    if local != world or torch.cuda.device_count() < world:
+        ok = False
+    else:
+        me = torch.cuda.current_device()
+        ok = all(torch.cuda.can_device_access_peer(me, d)
+                 for d in range(torch.cuda.device_count()) if d != me)
+    t = torch.tensor([1 if ok else 0], device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
+def run_distributed(u, v, cfg=None, peer=None):
     """run() over torch.distributed ranks (NCCL): this rank's slice of the
     sample pairs (CUDA int64 tensors) -> distributed build -> sharded
     coreness -> per-shard compaction -> the core gathered to every rank ->
     Greedy++ replica (dg_run_pruned).  Same RunResult as run() on the graph
-    of all pairs."""
+    of all pairs.  peer=None picks the peer-memory exchange when every rank
+    can map every other's memory (peer_capable), else NCCL all-to-all."""
     import torch
     from . import Graph, RunConfig, run_pruned
     from .sharded import CudaShard, TorchComm
     cfg = cfg or RunConfig()
     comm = TorchComm(torch.device("cuda", torch.cuda.current_device()))
+    if peer is None:
+        peer = peer_capable()
     offs, adj, orig, lab, kmax, rounds = prune_distributed([(u, v)], comm, CudaShard.from_rows,
-                                                           cfg, peer=True)
+                                                           cfg, peer=peer)
     return run_pruned(Graph.from_device_csr(offs, adj, orig), lab.cpu().numpy(), kmax, rounds,
                       cfg)

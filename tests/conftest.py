@@ -16,10 +16,11 @@ def pytest_configure(config):
 
 
 def _ensure_oracle():
-    so = os.path.join(ROOT, "oracle", "liboracle.so")
-    if not os.path.exists(so):
-        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), so], check=True,
-                       stdout=subprocess.DEVNULL)
+    for name in ("liboracle.so", "liboracle_par.so"):
+        so = os.path.join(ROOT, "oracle", name)
+        if not os.path.exists(so):
+            subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), so], check=True,
+                           stdout=subprocess.DEVNULL)
 
 
 @pytest.fixture(scope="session")
