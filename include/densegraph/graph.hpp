@@ -5,6 +5,7 @@
 // Like the reference's, a Graph is immutable after construction.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <span>

@@ -265,6 +265,15 @@ dg_status dg_gen_rmat(uint32_t scale, uint64_t samples, uint64_t seed, uint64_t*
 dg_status dg_gen_chung_lu(uint64_t n, uint64_t pairs, double n_root11, uint64_t seed,
                           uint64_t* u, uint64_t* v, int on_device);
 
+/* Exhaustive densest subgraph over all nonempty vertex subsets (the
+ * reference's test oracle, oracle.hpp:16-19 / oracle.cpp:70-108), on the
+ * device.  Ties: fewer vertices, then the lexicographically smallest id set.
+ * Outputs the reduced density and the witness as ORIGINAL ids, ascending
+ * (`witness` may be null; it needs room for n ids).  DG_E_EMPTY on n = 0,
+ * DG_E_ORACLE_SIZE when n > limit (or n > 32). */
+dg_status dg_brute_force_densest(const dg_graph* g, uint32_t limit, uint64_t* edges,
+                                 uint64_t* verts, uint64_t* witness, uint64_t* witness_n);
+
 /* Device memory helpers for callers that keep inputs resident in HBM. */
 dg_status dg_device_alloc(uint64_t bytes, void** ptr);
 dg_status dg_device_free(void* ptr);

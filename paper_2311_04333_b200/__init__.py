@@ -524,6 +524,23 @@ class RunResult:
     device_ms: float = 0.0
 
 
+@dataclass
+class OracleResult:
+    rho_star: Density
+    witness: np.ndarray  # original ids, ascending
+
+
+def brute_force_densest(g: Graph, limit: int = 22) -> OracleResult:
+    """oracle.hpp:16-19: exhaustive search over every nonempty subset (device
+    kernel, <= 32 vertices); ties -> fewer vertices, then the lexicographically
+    smallest id set.  EmptyGraphError / OracleSizeError as the reference."""
+    e, v, k = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    w = np.zeros(max(1, g.n), np.uint64)
+    _chk(LIB.dg_brute_force_densest(g._h, limit, C.byref(e), C.byref(v),
+                                    w.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(k)))
+    return OracleResult(Density(e.value, v.value), w[:k.value].copy())
+
+
 def set_device(device: int) -> None:
     _chk(LIB.dg_set_device(device))
 

@@ -98,6 +98,7 @@ PROTOTYPES = {
                               C.c_int]),
     "dg_gen_chung_lu": (C.c_int, [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, C.c_void_p,
                                   C.c_void_p, C.c_int]),
+    "dg_brute_force_densest": (C.c_int, [GP, C.c_uint32, u64p, u64p, u64p, u64p]),
     "dg_device_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "dg_device_free": (C.c_int, [C.c_void_p]),
     "dg_memcpy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int]),

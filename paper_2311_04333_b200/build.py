@@ -64,7 +64,46 @@ def build(verbose: bool = True, extra=(), tag: str = "") -> str:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
         if verbose:
             print(f"[build] linked {lib}", flush=True)
+    if not tag:
+        build_cli(lib, verbose)
     return lib
+
+
+CLI_SRC = os.path.join(PKG, "cli", "densest.cpp")
+CLI_BIN = os.path.join(PKG, "densest")
+
+
+def _json_include():
+    """nlohmann/json.hpp (the JSON library the reference CLI uses) as vendored
+    in the image's cudnn_frontend package."""
+    import glob
+    import site
+    roots = site.getsitepackages() + [os.path.join(sys.prefix, "lib")]
+    for r in roots:
+        for h in glob.glob(os.path.join(r, "**", "nlohmann", "json.hpp"), recursive=True):
+            return os.path.dirname(os.path.dirname(h))
+    return None
+
+
+def build_cli(lib: str, verbose: bool = True) -> str:
+    """The `densest` CLI (cli/densest.cpp, the reference's tools/densest.cpp
+    front end) against include/ and libdg_b200.so."""
+    deps = [CLI_SRC, lib] + [os.path.join(ROOT, "include", "densegraph", f)
+                             for f in os.listdir(os.path.join(ROOT, "include", "densegraph"))]
+    if os.path.exists(CLI_BIN) and os.path.getmtime(CLI_BIN) >= max(map(os.path.getmtime, deps)):
+        return CLI_BIN
+    inc = _json_include()
+    if inc is None:
+        raise RuntimeError("nlohmann/json.hpp not found: cannot build the densest CLI")
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cmd = [cxx, "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), "-I", inc, CLI_SRC,
+           "-o", CLI_BIN, "-L", PKG, "-ldg_b200", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stderr[-4000:]}")
+    if verbose:
+        print(f"[build] {CLI_BIN}", flush=True)
+    return CLI_BIN
 
 
 if __name__ == "__main__":

@@ -271,7 +271,10 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t x, uint32_t src) {
 // BM: liveness from an alive bitmap (n bits, cleared at labelling): arcs to
 // removed vertices skip the random read of deg, and a warp's tests of a
 // sorted neighbour list share sectors.
-template <bool BM>
+// PROF: the diagnostic variant (dg_kcore_profile, DG_KCORE_PROFILE=1) records
+// block-0 phase cycles and a per-round trace; the production variant has none
+// of that code.
+template <bool BM, bool PROF>
 __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -291,9 +294,9 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
   uint64_t Ftot = 0;
   uint64_t guard = 0;
   const bool P = blockIdx.x == 0 && threadIdx.x == 0;
-  long long pr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tp = clock64();
+  long long pr[8] = {}, tp = PROF ? clock64() : 0;
   auto mark = [&](int k) {
-    if (P) {
+    if (PROF && P) {
       const long long tt = clock64();
       pr[k] += tt - tp;
       tp = tt;
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       mark(0);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
       mark(1);
-      if (P) ++pr[6];
+      if (PROF && P) ++pr[6];
       const uint64_t gmin = s.b_minv;
       if (gmin == kUnset) {  // remaining > 0 but nothing alive: inconsistent
         if (P) a.out[2] = 2;
@@ -505,7 +508,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       }
     }
     __syncthreads();
-    if (P && a.rtrace && rounds <= 4096) {
+    if (PROF && P && rounds <= 4096) {
       a.rtrace[3 * (rounds - 1)] = clock64() - tp;
       a.rtrace[3 * (rounds - 1) + 1] = Fc;
       a.rtrace[3 * (rounds - 1) + 2] = Ftot;
@@ -526,7 +529,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     mark(5);
     ++f;
     if (s.b_ovf) {
-      if (P) ++pr[7];
+      if (PROF && P) ++pr[7];
       collect<BM>(a, livec, implicit, lv ? a.live1 : a.live0, lv ? a.live0 : a.live1, uint32_t(bound),
               uint32_t(label), a.fr[f & 1], nacc, s, &nacc->live);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, nacc); })) break;
@@ -542,7 +545,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     a.out[0] = kmax;
     a.out[1] = rounds;
     if (ld_relaxed_u32(&a.bar->abort)) a.out[2] = 4;
-    if (a.prof)
+    if (PROF)
       for (int k = 0; k < 8; ++k) a.prof[k] = pr[k];
   }
 }
@@ -621,7 +624,9 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   DG_CHECK_LAUNCH();
 
   const size_t smem = sizeof(Smem);
-  void* kfn = bm ? (void*)k_coreness<true> : (void*)k_coreness<false>;
+  const bool prof = getenv("DG_KCORE_PROFILE") && getenv("DG_KCORE_PROFILE")[0] == '1';
+  void* kfn = bm ? (prof ? (void*)k_coreness<true, true> : (void*)k_coreness<true, false>)
+                 : (prof ? (void*)k_coreness<false, true> : (void*)k_coreness<false, false>);
   DG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int occ = 0;
   DG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, KC_THREADS, smem));
@@ -642,8 +647,8 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
               acc.get(),
               bar.get(),
               out.get(),
-              kcore_prof_buffer() + 8,
-              kcore_prof_buffer(),
+              prof ? kcore_prof_buffer() + 8 : nullptr,
+              prof ? kcore_prof_buffer() : nullptr,
               approx ? 1 : 0,
               c_num,
               c_den};

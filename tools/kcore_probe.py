@@ -1,6 +1,8 @@
 """k-core phase split: python tools/kcore_probe.py [scale | bench config name]"""
 import ctypes as C
 import os
+os.environ["DG_KCORE_PROFILE"] = "1"  # the instrumented k-core variant
+import os
 import sys
 
 import numpy as np
