@@ -285,7 +285,8 @@ dg_status dg_set_device(int device);
 /* Number of this library's own kernels launched so far in this process. */
 uint64_t dg_launch_count(void);
 /* Return every cached block of the library's private device memory pool to
- * the driver (the pool keeps up to 16 GiB of freed scratch between calls). */
+ * the driver (the pool keeps freed blocks while it holds at most half the
+ * device memory). */
 dg_status dg_trim_memory(void);
 /* Evict L2 by writing a 256 MiB scratch buffer (bench hygiene between steps). */
 dg_status dg_flush_l2(void);
@@ -318,7 +319,8 @@ dg_status dg_peel_trace_read(uint64_t out[8 * 32 * 12]);
 /* Diagnostic: block-0 cycles of the last coreness launch in level-advance min
  * scans, level-advance barriers, collects, expansion, flushes, expansion
  * barriers; #level advances; #overflow collects. */
-dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]);  /* + per-round trace */
+#define DG_KCORE_PROFILE_WORDS (8 + 6 * 4096)
+dg_status dg_kcore_profile(uint64_t out[DG_KCORE_PROFILE_WORDS]); /* + per-round and per-level traces */
 /* Tuning / testing knob for the Greedy++ ordering kernel: 0 automatic (batch
  * mode: the thread-block cluster kernel for cores above 16K vertices, the
  * candidate-list kernel when no cluster fits; then the scanning single-CTA

@@ -19,7 +19,6 @@ namespace {
 constexpr int kMaxDev = 64;
 cudaStream_t g_streams[kMaxDev] = {};
 cudaMemPool_t g_pools[kMaxDev] = {};
-constexpr uint64_t kPoolKeep = 16ULL << 30;
 int g_sms[kMaxDev] = {};
 std::mutex g_mu;
 thread_local std::string g_err;
@@ -48,15 +47,17 @@ cudaStream_t stream() {
       g_sms[d] = p.multiProcessorCount;
       // A PRIVATE stream-ordered pool: the device's default pool (which torch,
       // NCCL and other users of cudaMallocAsync share) keeps its settings.
-      // Freed blocks stay cached up to kPoolKeep bytes (a run's scratch is
-      // reused by the next run); beyond that the pool returns memory to the
-      // driver at the next synchronisation, and dg_trim_memory releases all.
+      // Freed blocks stay cached while the pool holds at most half the
+      // device (a graph and a run's scratch are reused by the next call
+      // without re-mapping; RMAT-26's CSR alone is 8.9 GB); beyond that the
+      // pool returns memory to the driver at the next synchronisation, and
+      // dg_trim_memory releases everything.
       cudaMemPoolProps props = {};
       props.allocType = cudaMemAllocationTypePinned;
       props.location.type = cudaMemLocationTypeDevice;
       props.location.id = d;
       DG_CUDA(cudaMemPoolCreate(&g_pools[d], &props));
-      uint64_t thr = std::min<uint64_t>(kPoolKeep, p.totalGlobalMem / 8);
+      uint64_t thr = p.totalGlobalMem / 2;
       DG_CUDA(cudaMemPoolSetAttribute(g_pools[d], cudaMemPoolAttrReleaseThreshold, &thr));
       DG_CUDA(cudaStreamCreateWithFlags(&g_streams[d], cudaStreamNonBlocking));
     }

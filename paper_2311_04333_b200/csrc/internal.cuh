@@ -56,7 +56,7 @@ struct CoreOut {
 CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
                  uint32_t* d_labels);
 // block-0 cycle split of the last coreness launch (diagnostic)
-void kcore_profile(unsigned long long out[8 + 3 * 4096]);
+void kcore_profile(unsigned long long out[DG_KCORE_PROFILE_WORDS]);
 
 // ---- peel.cu ----
 struct KeyRange {

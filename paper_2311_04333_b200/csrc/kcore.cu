@@ -38,8 +38,9 @@ namespace {
 
 constexpr int KC_THREADS = 1024;
 constexpr uint32_t CH = 32;     // arcs per chunk = one warp step
-constexpr int UC = 2;           // chunks in flight per warp
-constexpr uint32_t BUF = 4096;  // per-CTA crossing buffer
+constexpr int UC = 2;           // chunks in flight per warp (short-row steps)
+constexpr int SC = 8;           // chunks per super-chunk (one warp step on long rows)
+constexpr uint32_t BUF = 8192;  // per-CTA crossing buffer
 constexpr uint32_t kUnset = 0xffffffffu;
 constexpr uint64_t M36 = (1ULL << 36) - 1;
 
@@ -73,21 +74,21 @@ struct KcArgs {
   Acc* acc;  // [3]
   GridBarrier* bar;
   uint32_t* out;               // kmax, rounds, err
-  unsigned long long* rtrace;  // [3*4096] per-round expand cycles, Fc, Ftot (diagnostic)
+  unsigned long long* rtrace;  // [3*4096] per-round expand cycles, Fc, Ftot, then
+                               // [3*4096] per-level-pass cycles, live entries, spilled (diagnostic)
   unsigned long long* prof;    // [8] block-0 cycles (see dg_kcore_profile)
   int approx;
   uint64_t c_num, c_den;
 };
 
 struct Smem {
-  uint32_t id[BUF];
-  uint32_t dg[BUF];
-  uint64_t of[BUF];
+  uint32_t id[BUF];  // staged vertices (next frontier / level-advance candidates)
   uint32_t rd[BUF];  // residual degree of a level-advance candidate
   uint64_t tileA[KC_THREADS];
   uint64_t ws[33];
   uint32_t ws32[33];
   uint32_t cnt;
+  uint32_t cmin;  // running CTA minimum of a level pass (exact mode)
   unsigned long long baseF, baseL;
   // phase scalars fetched by thread 0 after each grid barrier
   uint32_t abort;
@@ -195,7 +196,7 @@ __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const ui
 template <bool BM, int E>
 __device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint32_t* live_in,
                                            uint32_t* live_out, uint32_t livec, bool implicit,
-                                           uint64_t win, Acc* acc, uint32_t& lmin) {
+                                           uint64_t win, bool track, Acc* acc, uint32_t& lmin) {
   const uint32_t lane = lane_id();
   const uint64_t tile = uint64_t(blockDim.x) * E;
   const uint64_t stride = uint64_t(gridDim.x) * tile;
@@ -219,9 +220,12 @@ __device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint3
       d[e] = kUnset;
       if (i0 + e < livec) {
         const uint32_t x = v[e];
+        // the degree is read alongside the liveness word (not after it): one
+        // dependent round trip per entry instead of two
+        const uint32_t dx = a.deg[x];
         alive[e] = BM ? ((ld_relaxed_u32(&a.alive[x >> 5]) >> (x & 31)) & 1u) != 0
                       : a.labels[x] == kUnset;
-        if (alive[e]) d[e] = a.deg[x];
+        if (alive[e]) d[e] = dx;
       }
     }
     uint32_t c = 0;
@@ -230,14 +234,28 @@ __device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint3
       lmin = min(lmin, d[e]);
       c += alive[e];
       bool spill = false;
-      if (alive[e] && d[e] <= win) {
-        const uint32_t slot = atomicAdd(&s.cnt, 1u);
+      bool near;
+      if (track) {
+        // exact mode: the next bound IS the global minimum, so a CTA stages
+        // only vertices at its running minimum (entries staged before the
+        // minimum dropped are filtered at emission)
+        const uint32_t wm = __reduce_min_sync(~0u, alive[e] ? d[e] : kUnset);
+        if (lane == 0 && wm < *reinterpret_cast<volatile uint32_t*>(&s.cmin))
+          atomicMin(&s.cmin, wm);
+        __syncwarp();
+        near = alive[e] && d[e] <= *reinterpret_cast<volatile uint32_t*>(&s.cmin);
+      } else {
+        near = alive[e] && d[e] <= win;
+      }
+      const uint32_t nm = __ballot_sync(~0u, near);  // one shared atomic per warp
+      uint32_t nb = 0;
+      if (nm && lane == uint32_t(__ffs(nm) - 1)) nb = atomicAdd(&s.cnt, uint32_t(__popc(nm)));
+      if (nm) nb = __shfl_sync(~0u, nb, __ffs(nm) - 1);
+      if (near) {
+        const uint32_t slot = nb + __popc(nm & ((1u << lane) - 1u));
         if (slot < BUF) {
-          const uint64_t o0 = a.offs[v[e]];
           s.id[slot] = v[e];
           s.rd[slot] = d[e];
-          s.of[slot] = o0;
-          s.dg[slot] = uint32_t(a.offs[v[e] + 1] - o0);
         } else {
           spill = true;
         }
@@ -266,6 +284,110 @@ __device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint3
 // 64-bit warp shuffle
 __device__ __forceinline__ uint64_t shfl64(uint64_t x, uint32_t src) {
   return __shfl_sync(~0u, x, src);
+}
+
+
+// Liveness tests and decrements of K targets per lane (kUnset = none), all
+// K loads in flight before any atomic; a decrement that lands the degree
+// on the bound enrols the vertex in the next frontier (warp-aggregated slot
+// in the CTA's crossing buffer).
+template <bool BM, int K>
+__device__ __forceinline__ void expand_targets(const KcArgs& a, const uint32_t (&u)[K],
+                                               uint32_t b32, Smem& s, Acc* nacc) {
+  bool live[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint32_t uv = u[k];
+    live[k] = false;
+    if (uv == kUnset) continue;
+    if (BM)
+      live[k] = ((ld_relaxed_u32(&a.alive[uv >> 5]) >> (uv & 31)) & 1u) != 0;  // removed?
+    else
+      live[k] = a.deg[uv] > b32;  // dead, or already at/below the bound
+  }
+  uint32_t old[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) old[k] = live[k] ? atomicSub(&a.deg[u[k]], 1u) : 0u;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const bool cross = live[k] && old[k] == b32 + 1;  // crossed: joins the next round
+    const uint32_t cm = __ballot_sync(~0u, cross);
+    if (!cm) continue;
+    uint32_t base = 0;
+    if (lane_id() == __ffs(cm) - 1) base = atomicAdd(&s.cnt, uint32_t(__popc(cm)));
+    base = __shfl_sync(~0u, base, __ffs(cm) - 1);
+    if (cross) {
+      const uint32_t slot = base + __popc(cm & ((1u << lane_id()) - 1u));
+      const uint32_t uv = u[k];
+      if (slot < BUF) {
+        s.id[slot] = uv;  // its row is looked up at emission, off this critical path
+      } else {
+        nacc->ovf = 1;  // left unlabelled; the overflow collect finds it
+      }
+    }
+  }
+}
+
+// UC 32-arc chunks cb, cb + cs, ... (those below cend) of frontier F (nch
+// chunks in all): each chunk's entry window is loaded coalesced and a 5-step
+// shuffle search maps lanes to entries (no memory in the dependent chain).
+template <int UC_>
+__device__ __forceinline__ void load_chunks(const Frontier& F, const uint32_t* adj, uint64_t cb,
+                                            uint64_t cs, uint64_t cend, uint32_t Fc,
+                                            uint64_t Ftot, uint32_t lane, uint32_t (&u)[UC_],
+                                            uint64_t nch = 0) {
+  if (nch == 0) nch = cend;
+  uint32_t ne[UC_];
+  uint64_t e0[UC_], fa[UC_], fo[UC_];
+#pragma unroll
+  for (int k = 0; k < UC_; ++k) {
+    const uint64_t c = cb + k * cs;
+    ne[k] = 0;
+    e0[k] = 0;
+    fa[k] = ~0ULL;
+    fo[k] = 0;
+    if (c < cend) {
+      e0[k] = F.cse[c];
+      const uint64_t e1 = (c + 1 < nch) ? F.cse[c + 1] : uint64_t(Fc) - 1;
+      ne[k] = uint32_t(e1 - e0[k] + 1);
+      // rows of degree >= 1 need at most 32 entries for 32 arcs; only
+      // zero-degree rows can push the window past 32 (slow path)
+      if (ne[k] > 32 && F.fa[e0[k] + 32] > c * CH + CH - 1) ne[k] = 32;
+      if (lane < ne[k]) {
+        fa[k] = F.fa[e0[k] + lane];
+        fo[k] = F.fo[e0[k] + lane];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < UC_; ++k) {
+    const uint64_t c = cb + k * cs;
+    const uint64_t x = c * CH + lane;
+    u[k] = kUnset;
+    if (c >= cend) continue;  // warp-uniform
+    uint64_t p;
+    if (ne[k] <= 32) {
+      uint32_t l = 0;  // largest l < ne with fa[l] <= x
+#pragma unroll
+      for (uint32_t step = 16; step; step >>= 1) {
+        const uint32_t tl = l + step;
+        const uint64_t fl = __shfl_sync(~0u, fa[k], tl < 32 ? tl : 31);
+        if (tl < ne[k] && fl <= x) l = tl;
+      }
+      p = __shfl_sync(~0u, fo[k], l) + (x - __shfl_sync(~0u, fa[k], l));
+    } else {  // > 32 entries touch 32 arcs (zero-degree rows): binary search
+      uint64_t lo = e0[k], hi = e0[k] + ne[k] - 1;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi + 1) >> 1;
+        if (F.fa[mid] <= x)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      p = F.fo[lo] + (x - F.fa[lo]);
+    }
+    if (x < Ftot) u[k] = adj[p];
+  }
 }
 
 // BM: liveness from an alive bitmap (n bits, cleared at labelling): arcs to
@@ -318,14 +440,18 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       const uint32_t* live_in = lv ? a.live1 : a.live0;
       uint32_t* live_out = lv ? a.live0 : a.live1;
       const uint64_t win = bound + LW;
-      if (threadIdx.x == 0) s.cnt = 0;
+      const bool track = !a.approx;
+      if (threadIdx.x == 0) {
+        s.cnt = 0;
+        s.cmin = kUnset;
+      }
       __syncthreads();
       uint32_t lmin = kUnset;
       // wide tiles only while the list fills the grid LE times over
       if (livec >= uint64_t(gridDim.x) * blockDim.x * LE)
-        level_pass<BM, LE>(a, s, live_in, live_out, livec, implicit, win, acc, lmin);
+        level_pass<BM, LE>(a, s, live_in, live_out, livec, implicit, win, track, acc, lmin);
       else
-        level_pass<BM, 1>(a, s, live_in, live_out, livec, implicit, win, acc, lmin);
+        level_pass<BM, 1>(a, s, live_in, live_out, livec, implicit, win, track, acc, lmin);
       lmin = __reduce_min_sync(~0u, lmin);
       if (lane == 0) s.ws32[threadIdx.x >> 5] = lmin;
       __syncthreads();
@@ -334,9 +460,14 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
         x = __reduce_min_sync(~0u, x);
         if (threadIdx.x == 0 && x != kUnset) atomicMin(&acc->minv, x);
       }
+      if (PROF && P && pr[6] < 4096) {
+        a.rtrace[3 * 4096 + 3 * pr[6]] = clock64() - tp;
+        a.rtrace[3 * 4096 + 3 * pr[6] + 1] = livec;
+      }
       mark(0);
       if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
       mark(1);
+      if (PROF && P && pr[6] < 4096) a.rtrace[3 * 4096 + 3 * pr[6] + 2] = s.b_ccnt;
       if (PROF && P) ++pr[6];
       const uint64_t gmin = s.b_minv;
       if (gmin == kUnset) {  // remaining > 0 but nothing alive: inconsistent
@@ -359,15 +490,17 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       lv ^= 1;
       implicit = false;
       const Frontier& F0 = a.fr[f & 1];
-      if (bound <= win) {
+      if (track || bound <= win) {
         // the frontier = candidates with residual degree <= bound: this CTA's
         // staged ones, then a grid-strided share of the spilled ones
         const uint32_t cnt = min(s.cnt, BUF);
         for (uint32_t b0 = 0; b0 < cnt; b0 += blockDim.x) {
           const uint32_t i = b0 + threadIdx.x;
           const bool ok = i < cnt && s.rd[i] <= bound;
-          emit_front_tile(ok, ok ? s.id[i] : 0, ok ? s.dg[i] : 0, ok ? s.of[i] : 0,
-                          uint32_t(label), a, F0, acc, s);
+          const uint32_t v = ok ? s.id[i] : 0;
+          const uint64_t o = ok ? a.offs[v] : 0;
+          const uint32_t dl = ok ? uint32_t(a.offs[v + 1] - o) : 0;
+          emit_front_tile(ok, v, dl, o, uint32_t(label), a, F0, acc, s);
         }
         const uint64_t cc = s.b_ccnt;
         for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < cc;
@@ -428,81 +561,57 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       const Frontier& F = a.fr[f & 1];
       const uint32_t b32 = uint32_t(bound);
       const uint64_t nch = (Ftot + CH - 1) / CH;
-      for (uint64_t c0 = gwarp; c0 < nch; c0 += nwarps * UC) {
-        // stage UC chunks: entry window [e0, e0 + ne) per chunk, coalesced
-        uint32_t ne[UC];
-        uint64_t e0[UC], fa[UC], fo[UC];
-#pragma unroll
-        for (int k = 0; k < UC; ++k) {
-          const uint64_t c = c0 + uint64_t(k) * nwarps;
-          ne[k] = 0;
-          e0[k] = 0;
-          fa[k] = ~0ULL;
-          fo[k] = 0;
-          if (c < nch) {
-            e0[k] = F.cse[c];
-            const uint64_t e1 = (c + 1 < nch) ? F.cse[c + 1] : uint64_t(Fc) - 1;
-            ne[k] = uint32_t(e1 - e0[k] + 1);
-            // rows of degree >= 1 need at most 32 entries for 32 arcs; only
-            // zero-degree rows can push the window past 32 (slow path)
-            if (ne[k] > 32 && F.fa[e0[k] + 32] > c * CH + CH - 1) ne[k] = 32;
-            if (lane < ne[k]) {
-              fa[k] = F.fa[e0[k] + lane];
-              fo[k] = F.fo[e0[k] + lane];
-            }
-          }
+      // big rounds: one super-chunk = SC consecutive 32-arc chunks of the
+      // frontier's virtual arc space per warp step; rounds too small to give
+      // every warp two super-chunks keep one 32-arc chunk per step (UC in
+      // flight), so their work spreads over the whole grid
+      const bool wide = nch >= uint64_t(nwarps) * SC * 2;
+      const uint64_t nsc = wide ? (nch + SC - 1) / SC : 0;
+      if (!wide)
+        for (uint64_t cb = gwarp; cb < nch; cb += nwarps * UC) {
+          uint32_t u[UC];
+          load_chunks<UC>(F, a.adj, cb, nwarps, nch, Fc, Ftot, lane, u);
+          expand_targets<BM, UC>(a, u, b32, s, nacc);
         }
-        uint32_t u[UC];
-#pragma unroll
-        for (int k = 0; k < UC; ++k) {
-          const uint64_t c = c0 + uint64_t(k) * nwarps;
-          const uint64_t x = c * CH + lane;
-          u[k] = kUnset;
-          if (c >= nch) continue;  // warp-uniform
-          uint64_t p;
-          if (ne[k] <= 32) {
-            // largest l < ne with fa[l] <= x, by a shuffle search
-            uint32_t l = 0;
-#pragma unroll
-            for (uint32_t step = 16; step; step >>= 1) {
-              const uint32_t tl = l + step;
-              const uint64_t fl = shfl64(fa[k], tl < 32 ? tl : 31);
-              if (tl < ne[k] && fl <= x) l = tl;
-            }
-            p = shfl64(fo[k], l) + (x - shfl64(fa[k], l));
-          } else {  // > 32 entries touch 32 arcs (zero-degree rows): binary search
-            uint64_t lo = e0[k], hi = e0[k] + ne[k] - 1;
-            while (lo < hi) {
-              const uint64_t mid = (lo + hi + 1) >> 1;
-              if (F.fa[mid] <= x)
-                lo = mid;
-              else
-                hi = mid - 1;
-            }
-            p = F.fo[lo] + (x - F.fa[lo]);
+      for (uint64_t sc = gwarp; sc < nsc; sc += nwarps) {
+        const uint64_t c0 = sc * SC;
+        const uint64_t clast = min(c0 + SC, nch) - 1;
+        const uint64_t e0 = F.cse[c0];
+        const uint64_t e1 = (clast + 1 < nch) ? F.cse[clast + 1] : uint64_t(Fc) - 1;
+        if (e1 - e0 < 32) {
+          // <= 32 entries cover the super-chunk (rows average >= SC arcs):
+          // lane l holds entry e0 + l; SC independent adjacency loads, then SC
+          // liveness tests, then the decrements -- SC x the memory-level
+          // parallelism of one step per warp
+          const uint32_t ne = uint32_t(e1 - e0 + 1);
+          uint64_t fa = ~0ULL, fo = 0;
+          if (lane < ne) {
+            fa = F.fa[e0 + lane];
+            fo = F.fo[e0 + lane];
           }
-          if (x < Ftot) u[k] = a.adj[p];
-        }
+          uint32_t u[SC];
 #pragma unroll
-        for (int k = 0; k < UC; ++k) {
-          const uint32_t uv = u[k];
-          if (uv == kUnset) continue;
-          if (BM) {
-            if (!((ld_relaxed_u32(&a.alive[uv >> 5]) >> (uv & 31)) & 1u)) continue;  // removed
-          } else if (a.deg[uv] <= b32) {
-            continue;  // dead, or already at/below the bound
-          }
-          const uint32_t old = atomicSub(&a.deg[uv], 1u);
-          if (old == b32 + 1) {  // crossed: joins the next round
-            const uint32_t slot = atomicAdd(&s.cnt, 1u);
-            if (slot < BUF) {
-              const uint64_t o0 = a.offs[uv];
-              s.id[slot] = uv;
-              s.of[slot] = o0;
-              s.dg[slot] = uint32_t(a.offs[uv + 1] - o0);
-            } else {
-              nacc->ovf = 1;  // left unlabelled; the overflow collect finds it
+          for (int k = 0; k < SC; ++k) {
+            const uint64_t x = (c0 + k) * CH + lane;
+            uint32_t l = 0;  // largest l < ne with fa[l] <= x (every lane searches)
+            if (ne > 1) {    // warp-uniform
+#pragma unroll
+              for (uint32_t step = 16; step; step >>= 1) {
+                const uint32_t tl = l + step;
+                const uint64_t fl = shfl64(fa, tl < 32 ? tl : 31);
+                if (tl < ne && fl <= x) l = tl;
+              }
             }
+            const uint64_t p = shfl64(fo, l) + (x - shfl64(fa, l));
+            u[k] = x < Ftot ? a.adj[p] : kUnset;
+          }
+          expand_targets<BM, SC>(a, u, b32, s, nacc);
+        } else {
+          // many short rows: one 32-arc chunk per step, UC in flight
+          for (uint64_t cb = c0; cb <= clast; cb += UC) {
+            uint32_t u[UC];
+            load_chunks<UC>(F, a.adj, cb, 1, clast + 1, Fc, Ftot, lane, u, nch);
+            expand_targets<BM, UC>(a, u, b32, s, nacc);
           }
         }
       }
@@ -520,8 +629,10 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       for (uint32_t b0 = 0; b0 < cnt; b0 += blockDim.x) {
         const uint32_t i = b0 + threadIdx.x;
         const bool ok = i < cnt;
-        emit_front_tile(ok, ok ? s.id[i] : 0, ok ? s.dg[i] : 0, ok ? s.of[i] : 0,
-                        uint32_t(label), a, NF, nacc, s);
+        const uint32_t v = ok ? s.id[i] : 0;
+        const uint64_t o = ok ? a.offs[v] : 0;
+        const uint32_t dl = ok ? uint32_t(a.offs[v + 1] - o) : 0;
+        emit_front_tile(ok, v, dl, o, uint32_t(label), a, NF, nacc, s);
       }
     }
     mark(4);
@@ -577,14 +688,14 @@ unsigned long long* kcore_prof_buffer() {
   int d = 0;
   DG_CUDA(cudaGetDevice(&d));
   if (!buf[d]) {
-    DG_CUDA(cudaMalloc(&buf[d], (8 + 3 * 4096) * sizeof(unsigned long long)));
-    DG_CUDA(cudaMemset(buf[d], 0, (8 + 3 * 4096) * sizeof(unsigned long long)));
+    DG_CUDA(cudaMalloc(&buf[d], DG_KCORE_PROFILE_WORDS * sizeof(unsigned long long)));
+    DG_CUDA(cudaMemset(buf[d], 0, DG_KCORE_PROFILE_WORDS * sizeof(unsigned long long)));
   }
   return buf[d];
 }
 
-void kcore_profile(unsigned long long out[8 + 3 * 4096]) {
-  d2h(out, kcore_prof_buffer(), 8 + 3 * 4096);
+void kcore_profile(unsigned long long out[DG_KCORE_PROFILE_WORDS]) {
+  d2h(out, kcore_prof_buffer(), DG_KCORE_PROFILE_WORDS);
   stream_sync();
 }
 

@@ -256,11 +256,11 @@ extern "C" dg_status dg_peel_trace_read(uint64_t* out) {
   }
 }
 
-extern "C" dg_status dg_kcore_profile(uint64_t out[8 + 3 * 4096]) {
+extern "C" dg_status dg_kcore_profile(uint64_t out[DG_KCORE_PROFILE_WORDS]) {
   try {
-    static unsigned long long o[8 + 3 * 4096];
+    static unsigned long long o[DG_KCORE_PROFILE_WORDS];
     kcore_profile(o);
-    for (int i = 0; i < 8 + 3 * 4096; ++i) out[i] = o[i];
+    for (int i = 0; i < DG_KCORE_PROFILE_WORDS; ++i) out[i] = o[i];
     return DG_OK;
   } catch (const DgError& e) {
     return e.code;

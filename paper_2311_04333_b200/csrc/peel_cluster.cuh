@@ -54,6 +54,15 @@ constexpr int SB = 32;  // staged (small) batch members
 #endif
 // simple batches read only the CTA's slice of rows at least this long
 constexpr uint32_t kSliceMin = DG_SLICE_MIN;
+// DG_PEEL_PROF=1 (a tuning build: python build.py prof -DDG_PEEL_PROF=1)
+// records rank-0 phase cycles into Args::prof; the production kernel carries
+// none of those live registers.
+#ifndef DG_PEEL_PROF
+#define DG_PEEL_PROF 0
+#endif
+#ifndef DG_ROW_PREFETCH
+#define DG_ROW_PREFETCH 1
+#endif
 
 struct Args {
   const uint64_t* offs;
@@ -294,8 +303,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   uint32_t removed = 0, pos = 0, useB = 0;  // useB bit k: phase parity of mbB[k]
   bool marked = false;  // my chunk holds BATCH marks of the previous batch
   unsigned long long nbat = 0, nsimple = 0, nlarge = 0, clarge = 0, mlarge = 0;
-  const bool P = rank == 0 && tid == 0;
-  long long c1 = 0, c2 = 0, c3 = 0, tm = clock64();
+  const bool P = DG_PEEL_PROF && rank == 0 && tid == 0;
+  long long c1 = 0, c2 = 0, c3 = 0, tm = DG_PEEL_PROF ? clock64() : 0;
   while (removed < n) {
     const uint32_t par = uint32_t(nbat & 1);
     const uint32_t mbA = smem_u32(&s.mbA[par]), mbB = smem_u32(&s.mbB[par]);
@@ -354,6 +363,20 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           r1 = a.offs[gbase + f + 1];
         }
       }
+#if DG_ROW_PREFETCH
+      // the CTA's candidate is a likely member of this or an early batch:
+      // pull its row into L2 while the summaries travel (cores whose
+      // adjacency exceeds L2 -- RMAT-26's -- would otherwise pay an HBM
+      // round trip on the removal's critical path)
+      if (lane == 0 && R::alive(cm) && r1 > r0) {
+        const uint64_t b0 = (r0 * 4) & ~uint64_t(15);
+        const uint64_t b1 = min((r1 * 4 + 15) & ~uint64_t(15), b0 + (uint64_t(1) << 16));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                         reinterpret_cast<const char*>(a.adj) + b0),
+                     "r"(uint32_t(b1 - b0))
+                     : "memory");
+      }
+#endif
       if (lane < CS) {
         const uint32_t dst = mapa(smem_u32(&s.sum[par][rank]), lane);
         const uint32_t bar = mapa(mbA, lane);
@@ -386,7 +409,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     const uint32_t bs = a.one ? 1u : total;
     if (a.one || total == uint32_t(__popc(ownmask))) {
       // ---- simple batch: owner lane L (CTA L) holds member #(owners below L)
-      ++nsimple;
+      if (P) ++nsimple;
       const uint32_t rkl = __popc(ownmask & ((1u << lane) - 1u));
       // my CTA's member (if any): every warp marks it before its own
       // decrements (a later mark by another warp only rewrites a batch key)
@@ -534,8 +557,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     removed += bs;
     ++nbat;
   }
+  if (rank == 0 && tid == 0) *a.batches = nbat;
   if (P) {
-    *a.batches = nbat;
     if (a.prof) {
       a.prof[0] = c1;
       a.prof[1] = c2;

@@ -20,7 +20,7 @@ else:
     g = bench.device_graph(dg, bench.CONFIGS[arg])
 for _ in range(2):
     r = dg.run(g, dg.RunConfig(iterations=1))
-p = np.zeros(8 + 3 * 4096, np.uint64)
+p = np.zeros(8 + 6 * 4096, np.uint64)
 dg.LIB.dg_kcore_profile(p.ctypes.data_as(C.POINTER(C.c_uint64)))
 ghz = 1.965e3
 names = ["lvl_min", "lvl_sync", "collect", "expand", "flush", "exp_sync"]
@@ -39,3 +39,14 @@ for i in order[:8]:
 small = ftot < 4096
 print(f"  rounds with < 4096 arcs: {small.sum()} taking {cyc[small].sum()/ghz/1e3:.2f}ms "
       f"({cyc[small].mean()/ghz:.2f}us each); others {(~small).sum()} taking {cyc[~small].sum()/ghz/1e3:.2f}ms")
+
+L = int(p[6])
+lt = p[8 + 3 * 4096: 8 + 3 * 4096 + 3 * min(L, 4096)].reshape(-1, 3).astype(np.int64)
+lc, ll, lsp = lt[:, 0], lt[:, 1], lt[:, 2]
+print(f"  level passes: {L}, sum {lc.sum()/ghz/1e3:.3f}ms, entries scanned {ll.sum()/1e6:.1f}M, "
+      f"spilled {lsp.sum()/1e6:.2f}M")
+for lo, hi in ((0, 10), (10, 50), (50, 200), (200, 100000)):
+    sel = slice(lo, min(hi, L))
+    if lo < L:
+        print(f"    passes {lo}-{min(hi, L)}: {lc[sel].sum()/ghz/1e3:.3f}ms, mean live "
+              f"{ll[sel].mean():.0f}, mean {lc[sel].mean()/ghz:.2f}us/pass")
