@@ -262,6 +262,10 @@ dg_status dg_shard_finish_round(dg_shard* s, uint64_t* nnext);
  * on_device != 0, else host buffers of `samples` / `pairs` entries. */
 dg_status dg_gen_rmat(uint32_t scale, uint64_t samples, uint64_t seed, uint64_t* u, uint64_t* v,
                       int on_device);
+/* Samples [first, first + count) of the same RMAT stream (a rank's slice of
+ * a distributed input); u, v receive `count` entries. */
+dg_status dg_gen_rmat_range(uint32_t scale, uint64_t first, uint64_t count, uint64_t seed,
+                            uint64_t* u, uint64_t* v, int on_device);
 dg_status dg_gen_chung_lu(uint64_t n, uint64_t pairs, double n_root11, uint64_t seed,
                           uint64_t* u, uint64_t* v, int on_device);
 

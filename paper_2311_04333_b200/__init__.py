@@ -623,6 +623,20 @@ def gen_rmat(scale: int, samples: int, seed: int):
     return u, v
 
 
+def gen_rmat_range(scale: int, first: int, count: int, seed: int, device_ptrs=None):
+    """Samples [first, first + count) of the RMAT stream: a rank's slice of a
+    distributed input.  device_ptrs=(u_ptr, v_ptr) writes device buffers of
+    `count` u64 entries in place (e.g. torch tensors' data_ptr()); otherwise
+    host arrays are returned."""
+    if device_ptrs is not None:
+        _chk(LIB.dg_gen_rmat_range(scale, first, count, seed, device_ptrs[0], device_ptrs[1], 1))
+        return None
+    u = np.zeros(count, np.uint64)
+    v = np.zeros(count, np.uint64)
+    _chk(LIB.dg_gen_rmat_range(scale, first, count, seed, u.ctypes.data, v.ctypes.data, 0))
+    return u, v
+
+
 def gen_chung_lu(n: int, pairs: int, seed: int, n_root11: Optional[float] = None):
     R = float(n) ** (1.0 / 11.0) if n_root11 is None else n_root11
     u = np.zeros(pairs, np.uint64)

@@ -96,6 +96,8 @@ PROTOTYPES = {
     "dg_shard_finish_round": (C.c_int, [GP, u64p]),
     "dg_gen_rmat": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                               C.c_int]),
+    "dg_gen_rmat_range": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
+                                    C.c_void_p, C.c_int]),
     "dg_gen_chung_lu": (C.c_int, [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, C.c_void_p,
                                   C.c_void_p, C.c_int]),
     "dg_brute_force_densest": (C.c_int, [GP, C.c_uint32, u64p, u64p, u64p, u64p]),

@@ -756,6 +756,22 @@ dg_status dg_gen_rmat(uint32_t scale, uint64_t samples, uint64_t seed, uint64_t*
   DG_API_END
 }
 
+dg_status dg_gen_rmat_range(uint32_t scale, uint64_t first, uint64_t count, uint64_t seed,
+                            uint64_t* u, uint64_t* v, int on_device) {
+  DG_API_BEGIN
+  if (scale == 0 || scale > 32) throw DgError(DG_E_PARAM, "RMAT scale must be in 1..32");
+  if (on_device) {
+    gen_rmat_device(scale, count, seed, u, v, first);
+  } else {
+    DevBuf<uint64_t> du(count), dv(count);
+    gen_rmat_device(scale, count, seed, du.get(), dv.get(), first);
+    d2h(u, du.get(), count);
+    d2h(v, dv.get(), count);
+  }
+  stream_sync();
+  DG_API_END
+}
+
 dg_status dg_gen_chung_lu(uint64_t n, uint64_t pairs, double n_root11, uint64_t seed, uint64_t* u,
                           uint64_t* v, int on_device) {
   DG_API_BEGIN

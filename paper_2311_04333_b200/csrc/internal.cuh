@@ -103,7 +103,7 @@ void alg3(const dg_graph& g, const uint32_t* d_perm, const uint32_t* d_charges,
 
 // ---- gen.cu ----
 void gen_rmat_device(uint32_t scale, uint64_t samples, uint64_t seed, uint64_t* d_u,
-                     uint64_t* d_v);
+                     uint64_t* d_v, uint64_t first = 0);
 void gen_chung_lu_device(uint64_t n, uint64_t pairs, double R, uint64_t seed, uint64_t* d_u,
                          uint64_t* d_v);
 

@@ -43,17 +43,19 @@ def full(rep, cmd):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
-    h, v = r[0], r[2]
+    h = r[0]
     keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "lts__t_sector_hit_rate.pct", "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "smsp__warps_eligible.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
             "launch__grid_size", "launch__block_size"]
     print(f"ncu --set full --clock-control none --import-source on  {cmd}\n")
-    for k in keys:
-        if k in h:
-            print(f"{k}: {v[h.index(k)]} {r[1][h.index(k)]}")
-    print()
+    for li, v in enumerate(r[2:]):
+        print(f"-- launch {li}")
+        for k in keys:
+            if k in h:
+                print(f"{k}: {v[h.index(k)]} {r[1][h.index(k)]}")
+        print()
     print(det)
 
 
