@@ -254,6 +254,23 @@ dg_status dg_shard_peer_open(dg_shard* s, uint32_t rank, const void* handle /* 6
 dg_status dg_shard_peer_link(dg_shard* s, uint32_t rank, const dg_shard* other);
 dg_status dg_shard_expand_peer(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* produced);
 dg_status dg_shard_finish_round(dg_shard* s, uint64_t* nnext);
+/* Device-resident round loop: the whole sharded coreness as one
+ * persistent cooperative kernel per GPU.  `shards` are the shards THIS
+ * process holds (count = 1 per GPU on a multi-GPU job; any count on one GPU,
+ * each served by its own group of CTAs); every shard must be linked or opened
+ * to every other (peer mode) and all P shards must enter this call (one
+ * process per GPU: every rank calls it with its shard).  Rounds are separated
+ * by a flip barrier in shard 0's control block with system-scope atomics
+ * (NVLink peer memory across GPUs); remote decrements are atomicSub_system at
+ * the owner and a crossing appends the vertex to the owner's queue.  The
+ * caller resets shard 0's control block first (dg_shard_xctrl_reset, on the
+ * process holding shard 0) and makes every rank wait for that reset (e.g. a
+ * collective) before entering.  Labels are read with dg_shard_labels;
+ * kernel_ms (optional) is the launch's device time. */
+dg_status dg_shard_xctrl_reset(dg_shard* shard0);
+dg_status dg_shard_coreness_persistent(dg_shard** shards, uint32_t count, int approx,
+                                       uint64_t c_num, uint64_t c_den, uint32_t* kmax,
+                                       uint32_t* peel_rounds, float* kernel_ms);
 
 /* ------------------------------------------------------------ synthetic inputs */
 

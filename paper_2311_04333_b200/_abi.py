@@ -94,6 +94,10 @@ PROTOTYPES = {
     "dg_shard_peer_link": (C.c_int, [GP, C.c_uint32, GP]),
     "dg_shard_expand_peer": (C.c_int, [GP, C.c_uint32, C.c_uint32, u64p]),
     "dg_shard_finish_round": (C.c_int, [GP, u64p]),
+    "dg_shard_xctrl_reset": (C.c_int, [GP]),
+    "dg_shard_coreness_persistent": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, C.c_int,
+                                               C.c_uint64, C.c_uint64, C.POINTER(C.c_uint32),
+                                               C.POINTER(C.c_uint32), C.POINTER(C.c_float)]),
     "dg_gen_rmat": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                               C.c_int]),
     "dg_gen_rmat_range": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,

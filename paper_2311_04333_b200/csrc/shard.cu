@@ -18,37 +18,7 @@
 #include <cstring>
 #include <vector>
 
-#include "internal.cuh"
-
-// device view of one shard's peer block
-struct PeerView {
-  uint32_t* deg;
-  uint32_t* labels;
-  uint32_t* q[2];               // frontier queues (round parity)
-  unsigned long long* ctr;      // [2] queue counters
-};
-
-struct dg_shard {
-  uint64_t n = 0;  // global vertex count
-  uint64_t lo = 0, hi = 0;
-  dgb::DevBuf<uint64_t> offs;  // the rank's own rows: local offsets, n_local + 1
-  dgb::DevBuf<uint32_t> adj;   // neighbour ids (global dense ids)
-  void* block = nullptr;       // peer-visible state (cudaMalloc: IPC-exportable)
-  PeerView own{};
-  uint32_t cur = 0;            // queue holding the current frontier
-  dgb::DevBuf<unsigned long long> cnt;  // [0] next size, [1] min, [2..] per-rank counts
-  uint64_t nfront = 0;
-  dgb::DevBuf<uint64_t> bounds;  // rank boundaries (P + 1)
-  uint32_t P = 0;
-  std::vector<PeerView> peers;   // per rank (own entry included)
-  std::vector<void*> opened;     // IPC mappings to close
-  dgb::DevBuf<PeerView> d_peers;
-  bool peers_ready = false;
-  ~dg_shard() {
-    for (void* p : opened) cudaIpcCloseMemHandle(p);
-    if (block) cudaFree(block);
-  }
-};
+#include "shard.cuh"
 
 namespace dgb {
 namespace {
@@ -192,30 +162,16 @@ using namespace dgb;
 
 extern "C" {
 
-// common tail: state arrays, degree init
-// block layout: ctr u64[2] | deg | labels | q0 | q1 (u32[nl] each)
-static size_t block_bytes(uint64_t nl) { return 16 + 16 * (nl ? nl : 1); }
-static PeerView block_view(void* block, uint64_t nl) {
-  char* b = static_cast<char*>(block);
-  const uint64_t w = nl ? nl : 1;
-  PeerView v;
-  v.ctr = reinterpret_cast<unsigned long long*>(b);
-  v.deg = reinterpret_cast<uint32_t*>(b + 16);
-  v.labels = v.deg + w;
-  v.q[0] = v.labels + w;
-  v.q[1] = v.q[0] + w;
-  return v;
-}
-
 static void shard_init_state(dg_shard* s, const uint64_t* bounds, uint32_t P) {
   const uint64_t nl = s->hi - s->lo;
-  DG_CUDA(cudaMalloc(&s->block, block_bytes(nl)));
-  s->own = block_view(s->block, nl);
-  DG_CUDA(cudaMemsetAsync(s->own.ctr, 0, 16, stream()));
+  DG_CUDA(cudaMalloc(&s->block, shard_block_bytes(nl)));
+  s->own = shard_block_view(s->block, nl);
+  DG_CUDA(cudaMemsetAsync(s->block, 0, 128 + sizeof(XCtrl), stream()));
   s->peers.assign(P, PeerView{});
   s->cnt.alloc(2 + P);
   s->bounds.alloc(P + 1);
   h2d(s->bounds.get(), bounds, P + 1);
+  s->hbounds.assign(bounds, bounds + P + 1);
   if (nl) {
     k_sh_init<<<grid_for(nl, 256), 256, 0, stream()>>>(s->offs.get(), nl, s->own.deg,
                                                         s->own.labels);
@@ -241,6 +197,7 @@ dg_status dg_shard_create(const dg_graph* g, const uint64_t* bounds, uint32_t P,
   s->P = P;
   s->lo = bounds[rank];
   s->hi = bounds[rank + 1];
+  s->rank = rank;
   const uint64_t nl = s->hi - s->lo;
   // the rank's own rows (the source graph may be freed afterwards)
   s->offs.alloc(nl + 1);
@@ -272,6 +229,7 @@ dg_status dg_shard_create_rows(uint64_t n, const uint64_t* bounds, uint32_t P, u
   s->P = P;
   s->lo = bounds[rank];
   s->hi = bounds[rank + 1];
+  s->rank = rank;
   const uint64_t nl = s->hi - s->lo;
   uint64_t o[2] = {0, 0};
   if (on_device) {
@@ -391,12 +349,11 @@ dg_status dg_shard_apply(dg_shard* s, const uint32_t* d_recv, uint64_t nrecv, ui
 // ---- peer mode
 static void peer_set(dg_shard* s, uint32_t rank, void* block) {
   if (rank >= s->P) throw DgError(DG_E_PARAM, "peer rank out of range");
-  std::vector<uint64_t> b(s->P + 1);
-  d2h(b.data(), s->bounds.get(), s->P + 1);
-  stream_sync();
-  s->peers[rank] = block_view(block, b[rank + 1] - b[rank]);
+  s->peers[rank] = shard_block_view(block, s->hbounds[rank + 1] - s->hbounds[rank]);
   s->peers_ready = false;
 }
+
+
 
 dg_status dg_shard_ipc_handle(const dg_shard* s, void* handle) {
   DG_API_BEGIN
@@ -431,14 +388,7 @@ dg_status dg_shard_peer_link(dg_shard* s, uint32_t rank, const dg_shard* other) 
 dg_status dg_shard_expand_peer(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* produced) {
   DG_API_BEGIN
   if (!s || !produced) throw DgError(DG_E_PARAM, "null argument");
-  if (s->P > kMaxPeers) throw DgError(DG_E_PARAM, "peer mode supports at most 64 shards");
-  if (!s->peers_ready) {
-    for (const PeerView& v : s->peers)
-      if (!v.deg) throw DgError(DG_E_PARAM, "peer mode needs every rank linked or opened");
-    s->d_peers.alloc(s->P);
-    h2d(s->d_peers.get(), s->peers.data(), s->P);
-    s->peers_ready = true;
-  }
+  shard_device_peers(s);
   // the current queue's counter restarts: remote ranks append into this
   // queue only in the next round, after the round barrier
   DG_CUDA(cudaMemsetAsync(s->own.ctr + s->cur, 0, 8, stream()));
@@ -470,3 +420,17 @@ dg_status dg_shard_labels(const dg_shard* s, uint32_t* labels) {
 }
 
 }  // extern "C"
+
+namespace dgb {
+const PeerView* shard_device_peers(dg_shard* s) {
+  if (s->P > 64) throw DgError(DG_E_PARAM, "peer mode supports at most 64 shards");
+  if (!s->peers_ready) {
+    for (const PeerView& v : s->peers)
+      if (!v.deg) throw DgError(DG_E_PARAM, "peer mode needs every rank linked or opened");
+    s->d_peers.alloc(s->P);
+    h2d(s->d_peers.get(), s->peers.data(), s->P);
+    s->peers_ready = true;
+  }
+  return s->d_peers.get();
+}
+}  // namespace dgb

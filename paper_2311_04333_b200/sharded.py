@@ -369,6 +369,37 @@ def sharded_coreness(shards: List, comm, n_global: int, approx=None, peer: bool 
     return [s.labels() for s in shards], kmax, rounds
 
 
+def sharded_coreness_persistent(shards: List, comm, n_global: int, approx=None):
+    """The device-resident form of sharded_coreness(peer=True): every rank
+    launches ONE persistent kernel serving its shards (dg_shard_coreness_
+    persistent); rounds are separated by a cross-shard barrier in device
+    memory, so the host does no per-round work.  Shards must be linked
+    (link_local / link_ipc).  Returns (labels per local shard, kmax, rounds,
+    kernel ms)."""
+    from . import _chk
+    from ._abi import LIB
+    if approx is not None:
+        c_num, c_den = approx
+        if c_den == 0 or c_num <= c_den:
+            raise ValueError("approx_coreness needs c > 1")
+    else:
+        c_num, c_den = 1, 1
+    if comm.allreduce_sum(sum(s.n_local for s in shards)) != n_global:
+        raise ValueError("shards do not cover the graph")
+    if n_global == 0:
+        raise ValueError("coreness of empty graph")
+    for s in shards:
+        if s.rank == 0:
+            _chk(LIB.dg_shard_xctrl_reset(s._h))
+    comm.allreduce_sum(0)  # nobody enters before shard 0's control block is reset
+    hs = (C.c_void_p * len(shards))(*[s._h.value for s in shards])
+    kmax, rounds, ms = C.c_uint32(), C.c_uint32(), C.c_float()
+    _chk(LIB.dg_shard_coreness_persistent(hs, len(shards), 0 if approx is None else 1,
+                                          c_num, c_den, C.byref(kmax), C.byref(rounds),
+                                          C.byref(ms)))
+    return [s.labels() for s in shards], kmax.value, rounds.value, ms.value
+
+
 def _decomposition(labels, kmax, rounds, approx):
     from . import CoreDecomposition
     return CoreDecomposition(labels=labels, kmax=kmax, peel_rounds=rounds,
@@ -377,25 +408,34 @@ def _decomposition(labels, kmax, rounds, approx):
                              c_den=1 if approx is None else approx[1])
 
 
-def coreness_local_shards(g, P: int, approx=None, peer: bool = False):
-    """All P range shards of `g` on this GPU (validates the shard kernels)."""
+def coreness_local_shards(g, P: int, approx=None, peer: bool = False,
+                          persistent: bool = False):
+    """All P range shards of `g` on this GPU (validates the shard kernels).
+    persistent=True: one cooperative launch, a group of CTAs per shard."""
     bounds = partition(g.offs, P)
     shards = [CudaShard(g, bounds, r) for r in range(P)]
-    if peer:
+    if peer or persistent:
         link_local(shards)
+    if persistent:
+        labs, kmax, rounds, _ = sharded_coreness_persistent(shards, LocalComm(P), g.n, approx)
+        return _decomposition(np.concatenate(labs), kmax, rounds, approx)
     labs, kmax, rounds = sharded_coreness(shards, LocalComm(P), g.n, approx, peer)
     return _decomposition(np.concatenate(labs), kmax, rounds, approx)
 
 
-def coreness_distributed(g, approx=None, peer: bool = True):
+def coreness_distributed(g, approx=None, peer: bool = True, persistent: bool = False):
     """One range shard per torch.distributed rank (NCCL); every rank gets all
     labels.  peer=True maps the other ranks' shard state by CUDA IPC (one
-    node, NVLink) and runs the fused rounds."""
+    node, NVLink) and runs the fused rounds; persistent=True runs them as one
+    device-resident kernel per GPU (implies peer)."""
     import torch
     comm = TorchComm(torch.device("cuda", torch.cuda.current_device()))
     bounds = partition(g.offs, comm.P)
     shard = CudaShard(g, bounds, comm.rank)
-    if peer:
+    if peer or persistent:
         link_ipc(shard, comm)
+    if persistent:
+        labs, kmax, rounds, _ = sharded_coreness_persistent([shard], comm, g.n, approx)
+        return _decomposition(np.concatenate(comm.allgather(labs[0])), kmax, rounds, approx)
     labs, kmax, rounds = sharded_coreness([shard], comm, g.n, approx, peer)
     return _decomposition(np.concatenate(comm.allgather(labs[0])), kmax, rounds, approx)

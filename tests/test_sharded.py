@@ -252,6 +252,39 @@ def test_cuda_shards_peer_local(orc, dg, P):
             _check(orc, hg, [dec.labels], dec.kmax, dec.peel_rounds, approx)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 7, 16])
+def test_cuda_shards_persistent_local(orc, dg, P):
+    """The device-resident round loop (dg_shard_coreness_persistent): P
+    shards served by P CTA groups of ONE cooperative launch, rounds separated
+    by the cross-shard barrier in shard 0's control block, remote decrements
+    and queue appends through the peer views -- the code path every GPU of a
+    multi-GPU job runs with one group."""
+    from paper_2311_04333_b200.sharded import coreness_local_shards
+    for name, hg in _graphs(orc).items():
+        g = dg.Graph.from_csr(hg.offs, hg.adj, hg.orig)
+        for approx in APPROX:
+            dec = coreness_local_shards(g, P, approx, persistent=True)
+            _check(orc, hg, [dec.labels], dec.kmax, dec.peel_rounds, approx)
+
+
+@pytest.mark.gpu
+def test_cuda_shards_persistent_rmat(orc, dg):
+    """RMAT-18 (hub rows cut into pieces): 1, 4 and 8 shards in one launch
+    against the single-GPU kernel, exact and approximate."""
+    from paper_2311_04333_b200.sharded import coreness_local_shards
+    g = dg.Graph.generate_rmat(18, 16 << 18, 18)
+    one = dg.exact_coreness(g)
+    apx = dg.approx_coreness(g, 3, 2)
+    for P in (1, 4, 8):
+        dec = coreness_local_shards(g, P, persistent=True)
+        np.testing.assert_array_equal(dec.labels, one.labels)
+        assert (dec.kmax, dec.peel_rounds) == (one.kmax, one.peel_rounds)
+        dec = coreness_local_shards(g, P, (3, 2), persistent=True)
+        np.testing.assert_array_equal(dec.labels, apx.labels)
+        assert (dec.kmax, dec.peel_rounds) == (apx.kmax, apx.peel_rounds)
+
+
 def _ipc_worker(rank, world, port, outdir):
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
