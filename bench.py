@@ -119,11 +119,32 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ distributed plumbing
-def dist_init():
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: launch N ranks of this same
+    command line on this node (torchrun, 127.0.0.1) and return their status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dist_init(force: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world == 1 and force:  # the sharded pipeline on one rank (its own process group)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(free_port()))
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    if world > 1 or force:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -423,6 +444,116 @@ def run_ours(args, cfg, rank, world, local):
     return 0
 
 
+# ------------------------------------------------------------------ our arm, N GPUs
+def run_sharded(args, cfg, rank, world, local):
+    """The multi-GPU pipeline on the SAME graph (strong scaling):
+    every rank generates its slice of the seeded samples on its GPU ->
+    distributed CSR build (library kernels + NCCL all-to-all) -> sharded exact
+    k-core as ONE persistent kernel per GPU (peer memory over NVLink,
+    device-side cross-GPU barrier) -> per-shard get_core -> the core
+    all-gathered -> Greedy++ T iterations (replicated on every rank: one
+    exact minimum per batch does not shard).  A step is the whole
+    pipeline; times are CUDA events / device clocks, max over ranks."""
+    import numpy as np
+    import torch
+    import paper_2311_04333_b200 as dg
+    from paper_2311_04333_b200.sharded import CudaShard, TorchComm
+    from paper_2311_04333_b200.sharded_build import peer_capable, prune_distributed
+    if cfg["kind"] != "rmat":
+        raise SystemExit("the multi-GPU pipeline generates RMAT slices per rank (rmat* configs)")
+    dg.set_device(local)
+    dev = torch.device("cuda", local)
+    hbm, peak_kind = peaks()
+    S = cfg["edge_factor"] << cfg["scale"]
+    k0, k1 = S * rank // world, S * (rank + 1) // world
+    peer = peer_capable() if world > 1 else True
+    rcfg = dg.RunConfig(iterations=cfg["T"], epsilon=cfg["eps"])
+    comm = TorchComm(dev)
+
+    def step():
+        u = torch.empty(k1 - k0, dtype=torch.int64, device=dev)
+        v = torch.empty(k1 - k0, dtype=torch.int64, device=dev)
+        dg.gen_rmat_range(cfg["scale"], k0, k1 - k0, cfg["seed"], (u.data_ptr(), v.data_ptr()))
+        torch.cuda.synchronize(dev)
+        tm = {}
+        offs, adj, orig, lab, kmax, rounds = prune_distributed(
+            [(u, v)], comm, CudaShard.from_rows, rcfg, peer=peer, persistent=peer, timings=tm)
+        del u, v
+        r = dg.run_pruned(dg.Graph.from_device_csr(offs, adj, orig), lab.cpu().numpy(), kmax,
+                          rounds, rcfg)
+        return r, tm
+
+    for _ in range(args.warmup):
+        step()
+    clocks = Clocks(local)
+    time.sleep(0.25)
+    barrier(world)
+    t_start = time.time()
+    res, prune_s = [], []
+    launches0 = dg.launch_count()
+    for _ in range(args.steps):
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r, tm = step()
+        dg.synchronize()
+        torch.cuda.synchronize(dev)
+        e1.record()
+        e1.synchronize()
+        barrier(world)
+        res.append((r, tm, e0.elapsed_time(e1) / 1e3))  # device-observed seconds
+    t_end = time.time()
+    clk = clocks.summary(t_start, t_end)
+    clocks.stop()
+    launches = dg.launch_count() - launches0
+    iters = [it for r, _, _ in res for it in r.trace.iters]
+    edges = sum(it.m for it in iters)
+    it_ms = sum(it.ms for it in iters)
+    step_s = sum(x for _, _, x in res)
+    pr_s = sum(t["build_s"] + t["coreness_s"] + t["get_core_gather_s"] for _, t, _ in res)
+    kc_ms = sum(t["coreness_kernel_ms"] or 0.0 for _, t, _ in res)
+    bd_s = sum(t["build_s"] for _, t, _ in res)
+    it_ms_max, step_max, pr_max, kc_max, bd_max = allreduce([it_ms, step_s, pr_s, kc_ms, bd_s],
+                                                            "max", world, local)
+    r0, t0_ = res[0][0], res[0][1]
+    n, m = t0_["n"], t0_["m"]
+    kc_bytes = 8 * m + 16 * n + 8
+    line = {
+        "metric": METRIC, "value": edges / (it_ms_max / 1e3), "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step_max / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": dict(workload_config(args.config, cfg, n, m, world),
+                       parallelism=f"1D vertex-range shards x{world} (k-core), Greedy++ replicated",
+                       pipeline="per-rank generation -> distributed CSR build -> persistent sharded "
+                                "k-core -> per-shard get_core -> core all-gather -> Greedy++"),
+        "kcore": {"value": m * args.steps / (kc_max / 1e3) if kc_max else None, "unit": "edges/s",
+                  "ms": kc_max / args.steps,
+                  "kernel": "k_shard_coreness (one persistent kernel per GPU)",
+                  "roofline": {"bound": "hbm", "achieved": kc_bytes * args.steps / (kc_max / 1e3) / 1e9
+                               / world if kc_max else None, "peak": hbm, "unit": "GB/s",
+                               "frac": kc_bytes * args.steps / (kc_max / 1e3) / 1e9 / world / hbm
+                               if kc_max else None, "peak_kind": peak_kind,
+                               "note": "per GPU: algorithmic bytes / N / time"}},
+        "sharded": {"time_to_solution_ms": 1e3 * step_max / args.steps,
+                    "build_ms": 1e3 * bd_max / args.steps,
+                    "build_kcore_prune_gather_ms": 1e3 * pr_max / args.steps,
+                    "kcore_rounds": r0.trace.init.peel_rounds, "kmax": r0.trace.init.kmax,
+                    "peer_memory": bool(peer),
+                    "core_n_m": [r0.trace.init.pruned_n, r0.trace.init.pruned_m],
+                    "best": [r0.best.edges, r0.best.verts]},
+        "greedy": {"iterations": len(iters), "ms_per_iter": it_ms_max / max(1, len(iters))},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "value_note": "Greedy++ runs replicated on the gathered core: value counts one replica's "
+                      "edges (the others are redundant), time = max over ranks",
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def cpu_baseline(cfg, offs, adj, orig):
     from oracle import HostGraph, Reference, RunConfig, reference_available
     if not reference_available():
@@ -452,14 +583,23 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="rmat26", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-GPU pipeline even on one rank (tests its plumbing)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
-    rank, world, local = dist_init()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
+    sharded = args.impl == "ours" and (args.gpus > 1 or args.sharded)
+    rank, world, local = dist_init(force=sharded)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         rc = run_reference(args, cfg, rank, world)
+    elif sharded:
+        rc = run_sharded(args, cfg, rank, world, local)
     else:
         rc = run_ours(args, cfg, rank, world, local)
-    if world > 1:
+    if world > 1 or sharded:
         import torch.distributed as dist
         dist.destroy_process_group()
     return rc

@@ -254,6 +254,48 @@ dg_status dg_shard_peer_open(dg_shard* s, uint32_t rank, const void* handle /* 6
 dg_status dg_shard_peer_link(dg_shard* s, uint32_t rank, const dg_shard* other);
 dg_status dg_shard_expand_peer(dg_shard* s, uint32_t bound, uint32_t label, uint64_t* produced);
 dg_status dg_shard_finish_round(dg_shard* s, uint64_t* nnext);
+/* Distributed CSR build and per-shard get_core, the per-rank device steps
+ * (the caller moves buffers between ranks with its collectives; see
+ * paper_2311_04333_b200/sharded_build.py).  All array arguments are DEVICE
+ * pointers except `id_bounds`, `counts` and `hist` (host).  Original ids must
+ * be below 2^32.
+ *   max_id        largest endpoint of a non-loop pair (0: none)
+ *   endpoint_hist histogram of non-loop endpoints >> shift (nb <= 4096)
+ *   route         both arc directions of every non-loop pair as (src << 32 |
+ *                 dst) keys, grouped by the owner of src (original-id ranges
+ *                 [id_bounds[r], id_bounds[r+1])); counts[r] keys per owner
+ *   rows          received keys (sorted in place) -> unique -> rows: offs
+ *                 (nverts + 1), distinct sources `verts`, neighbour ids `dst`
+ *   unique        distinct values (ascending) and each entry's index into them
+ *   lookup        dense ids of asked original ids: base + position in verts
+ *   bucket_counts entries of ascending `vals` per owner range (host counts)
+ *   take          out[map[i] - base] = in[i] for kept i (4- or 8-byte elements)
+ *   relabel       adj[i] = back[inv[i]]
+ *   keep_map      map[i] = base + rank among labels >= k, UINT32_MAX if dropped
+ *   core_rows     rows of kept vertices, neighbours renamed through full_map
+ *                 (global old id -> new id), dropped ones removed in order */
+dg_status dg_dist_max_id(const uint64_t* u, const uint64_t* v, uint64_t k, uint64_t* out);
+dg_status dg_dist_endpoint_hist(const uint64_t* u, const uint64_t* v, uint64_t k, uint32_t shift,
+                                uint32_t nb, uint64_t* hist);
+dg_status dg_dist_route(const uint64_t* u, const uint64_t* v, uint64_t k,
+                        const uint64_t* id_bounds, uint32_t P, uint64_t* keys, uint64_t* counts);
+dg_status dg_dist_rows(uint64_t* keys, uint64_t n, uint64_t* offs, uint64_t* verts,
+                       uint32_t* dst, uint64_t* nverts, uint64_t* narcs);
+dg_status dg_dist_unique(const uint32_t* vals, uint64_t n, uint32_t* uniq, uint32_t* inv,
+                         uint64_t* nuniq);
+dg_status dg_dist_lookup(const uint64_t* verts, uint64_t nv, const uint32_t* asked, uint64_t na,
+                         uint64_t base, uint32_t* out);
+dg_status dg_dist_bucket_counts(const uint32_t* vals, uint64_t n, const uint64_t* id_bounds,
+                                uint32_t P, uint64_t* counts);
+dg_status dg_dist_take(const void* in, const uint32_t* map, uint64_t nl, uint64_t base,
+                       uint32_t elem_bytes, void* out);
+dg_status dg_dist_relabel(const uint32_t* back, const uint32_t* inv, uint64_t n, uint32_t* adj);
+dg_status dg_dist_keep_map(const uint32_t* labels, uint64_t nl, uint32_t k, uint64_t base,
+                           uint32_t* map, uint64_t* kept);
+dg_status dg_dist_core_rows(const uint64_t* offs, const uint32_t* adj, uint64_t nl,
+                            const uint32_t* local_map, const uint32_t* full_map,
+                            uint64_t* noffs, uint32_t* nadj, uint64_t* nkept, uint64_t* narcs);
+
 /* Device-resident round loop: the whole sharded coreness as one
  * persistent cooperative kernel per GPU.  `shards` are the shards THIS
  * process holds (count = 1 per GPU on a multi-GPU job; any count on one GPU,

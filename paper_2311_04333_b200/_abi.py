@@ -95,6 +95,24 @@ PROTOTYPES = {
     "dg_shard_expand_peer": (C.c_int, [GP, C.c_uint32, C.c_uint32, u64p]),
     "dg_shard_finish_round": (C.c_int, [GP, u64p]),
     "dg_shard_xctrl_reset": (C.c_int, [GP]),
+    "dg_dist_max_id": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
+    "dg_dist_endpoint_hist": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
+                                        C.c_uint32, u64p]),
+    "dg_dist_route": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_uint32,
+                                C.c_void_p, u64p]),
+    "dg_dist_rows": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                               u64p, u64p]),
+    "dg_dist_unique": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, u64p]),
+    "dg_dist_lookup": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint64,
+                                 C.c_void_p]),
+    "dg_dist_bucket_counts": (C.c_int, [C.c_void_p, C.c_uint64, u64p, C.c_uint32, u64p]),
+    "dg_dist_take": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                               C.c_void_p]),
+    "dg_dist_relabel": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "dg_dist_keep_map": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_void_p,
+                                   u64p]),
+    "dg_dist_core_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, u64p, u64p]),
     "dg_shard_coreness_persistent": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, C.c_int,
                                                C.c_uint64, C.c_uint64, C.POINTER(C.c_uint32),
                                                C.POINTER(C.c_uint32), C.POINTER(C.c_float)]),

@@ -12,11 +12,15 @@ import numpy as np
 import pytest
 import torch
 
+from dist_ops_torch import TorchDistOps
 from shard_numpy import NumpyShard
 from test_sharded import _free_port
 
 from paper_2311_04333_b200.sharded import LocalComm, TorchComm, sharded_coreness
 from paper_2311_04333_b200.sharded_build import build_shards
+
+
+HOST = TorchDistOps()  # host restatement of the CUDA steps (tests only)
 
 
 def _cases(orc):
@@ -78,7 +82,7 @@ def test_build_local_matches_oracle(orc, P):
     for name, (u, v) in _cases(orc).items():
         g = orc.build(u, v)
         for skew in (False, True):
-            n, bounds, sh = build_shards(_split(u, v, P, skew), LocalComm(P, "cpu"))
+            n, bounds, sh = build_shards(_split(u, v, P, skew), LocalComm(P, "cpu"), HOST)
             _check_csr(g, n, bounds, sh)
             # coreness over the rank-owned rows = the oracle's
             shards = [NumpyShard.from_rows(n, bounds, r, sh[r][0], sh[r][1]) for r in range(P)]
@@ -92,7 +96,7 @@ def test_build_balances_arcs(orc):
     u, v = orc.gen_rmat(14, 16 << 14, 8)
     g = orc.build(u, v)
     P = 4
-    n, bounds, sh = build_shards(_split(u, v, P), LocalComm(P, "cpu"))
+    n, bounds, sh = build_shards(_split(u, v, P), LocalComm(P, "cpu"), HOST)
     arcs = np.array([int(_np(o, np.uint64)[-1]) for o, _, _ in sh])
     assert arcs.sum() == int(g.offs[-1])
     # bucket-granular split: within 25% of the ideal share on RMAT-14
@@ -102,9 +106,12 @@ def test_build_balances_arcs(orc):
 def test_build_rejects_bad_input():
     z = torch.zeros(0, dtype=torch.int64)
     with pytest.raises(ValueError, match="no edges"):
-        build_shards([(torch.tensor([3, 4]), torch.tensor([3, 4])), (z, z)], LocalComm(2, "cpu"))
+        build_shards([(torch.tensor([3, 4]), torch.tensor([3, 4])), (z, z)], LocalComm(2, "cpu"),
+                     HOST)
     with pytest.raises(ValueError, match="2\\^32"):
-        build_shards([(torch.tensor([0]), torch.tensor([1 << 32]))], LocalComm(1, "cpu"))
+        build_shards([(torch.tensor([0]), torch.tensor([1 << 32]))], LocalComm(1, "cpu"), HOST)
+    with pytest.raises(ValueError, match="CUDA"):  # the product has no host path
+        build_shards([(torch.tensor([0]), torch.tensor([1]))], LocalComm(1, "cpu"))
 
 
 def _gloo_worker(rank, world, port, outdir):
@@ -120,7 +127,7 @@ def _gloo_worker(rank, world, port, outdir):
         res = {}
         for name, (u, v) in _cases(orc).items():
             comm = TorchComm("cpu")
-            n, bounds, sh = build_shards([_split(u, v, world)[rank]], comm)
+            n, bounds, sh = build_shards([_split(u, v, world)[rank]], comm, TorchDistOps())
             shard = NumpyShard.from_rows(n, bounds, rank, sh[0][0], sh[0][1])
             labs, kmax, rounds = sharded_coreness([shard], comm, n)
             parts = comm.allgather((sh[0], labs[0]))
@@ -209,7 +216,7 @@ def test_prune_local_matches_oracle(orc, P):
         g = orc.build(u, v)
         for pruning in PRUNINGS:
             got = prune_distributed(_split(u, v, P), LocalComm(P, "cpu"), NumpyShard.from_rows,
-                                    RunConfig(pruning=pruning))
+                                    RunConfig(pruning=pruning), ops=HOST)
             _check_core(orc, g, pruning, got)
 
 
@@ -219,7 +226,7 @@ def test_prune_rejects_none(orc):
     u, v = _cases(orc)["planted"]
     with pytest.raises(ValueError):
         prune_distributed(_split(u, v, 2), LocalComm(2, "cpu"), NumpyShard.from_rows,
-                          RunConfig(pruning="none"))
+                          RunConfig(pruning="none"), ops=HOST)
 
 
 def _gloo_prune_worker(rank, world, port, outdir):
@@ -238,7 +245,7 @@ def _gloo_prune_worker(rank, world, port, outdir):
             for pruning in PRUNINGS:
                 res[f"{name}/{pruning}"] = prune_distributed(
                     [_split(u, v, world)[rank]], TorchComm("cpu"), NumpyShard.from_rows,
-                    RunConfig(pruning=pruning))
+                    RunConfig(pruning=pruning), ops=TorchDistOps())
         np.save(os.path.join(outdir, f"res{rank}.npy"), res, allow_pickle=True)
     finally:
         dist.destroy_process_group()
@@ -273,7 +280,8 @@ def test_run_pruned_matches_run(orc, dg, P):
                 cfg = dg.RunConfig(algorithm=algorithm, pruning=pruning, iterations=6)
                 pairs = [(a.cuda(), b.cuda()) for a, b in _split(u, v, P)]
                 offs, adj, orig, lab, kmax, rounds = prune_distributed(
-                    pairs, LocalComm(P), CudaShard.from_rows, cfg, peer=(P > 1))
+                    pairs, LocalComm(P), CudaShard.from_rows, cfg, peer=(P > 1),
+                    persistent=(P > 1))
                 got = dg.run_pruned(dg.Graph.from_device_csr(offs, adj, orig),
                                     lab.cpu().numpy(), kmax, rounds, cfg)
                 want = dg.run(g, cfg)
