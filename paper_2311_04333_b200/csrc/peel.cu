@@ -414,7 +414,11 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
   const bool offs32 = 2 * g.m < 0xffffffffULL;
   bool offs_smem = offs32 && peelc::smem_bytes(sh, true) <= kSmemCap;
   if (!offs_smem && peelc::smem_bytes(sh, false) > kSmemCap) return false;
-  const size_t smem = peelc::smem_bytes(sh, offs_smem);
+  // every row's slice bounds in shared memory when they fit (rows < 2^16 arcs)
+  const bool slice_smem = PT == 512 && g.maxdeg < 65536 &&
+                          peelc::smem_bytes(sh, offs_smem, n) <= kSmemCap &&
+                          !getenv("DG_NO_SLICE_SMEM");
+  const size_t smem = peelc::smem_bytes(sh, offs_smem, slice_smem ? n : 0);
   auto kern = peelc::k_peel_cluster<CS, PT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess) {
@@ -451,8 +455,8 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
                                                                       sh, seg.get());
   DG_CHECK_LAUNCH();
   peelc::Args a{g.offs.get(), g.adj.get(), uint32_t(n), d_loads, base, one ? 1 : 0,
-                sh, (1u << sh) / PT, offs_smem ? 1 : 0, d_perm, d_raw, seg.get(), d_batches,
-                peel_prof_buffer()};
+                sh, (1u << sh) / PT, offs_smem ? 1 : 0, d_perm, d_raw, seg.get(),
+                slice_smem ? 1 : 0, d_batches, peel_prof_buffer()};
   DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   count_launch();
   return true;

@@ -79,6 +79,8 @@ struct Args {
   // seg[v*(CS+1) + r]: offset inside row v of its first neighbour owned by
   // CTA r (rows ascend, so CTA r's targets are [seg[r], seg[r+1]))
   const uint32_t* seg;
+  int slice_smem;  // this CTA's slice bounds of EVERY row staged in shared memory
+                   // (u16 start | u16 end << 16; rows shorter than 2^16)
   unsigned long long* batches;
   unsigned long long* prof;  // [8] rank-0 thread-0 cycles: S1, S2, S3, batches, simple
 };
@@ -265,8 +267,10 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   const uint32_t NC = 1u << a.sh;
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem);
   uint32_t* soffs = keys + NC;  // NC + 1 entries when staged
-  Fixed& s = *reinterpret_cast<Fixed*>(smem + ((size_t(NC) * 4 * (a.offs_smem ? 2 : 1) + 4 + 15) &
-                                              ~size_t(15)));
+  const size_t head = (size_t(NC) * 4 * (a.offs_smem ? 2 : 1) + 4 + 15) & ~size_t(15);
+  uint32_t* sslice = reinterpret_cast<uint32_t*>(smem + head);  // n entries when staged
+  Fixed& s = *reinterpret_cast<Fixed*>(
+      smem + head + (PT == 512 && a.slice_smem ? ((size_t(a.n) * 4 + 15) & ~size_t(15)) : 0));
   const uint4* adj4 = reinterpret_cast<const uint4*>(a.adj);
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
   const uint32_t n = a.n, c = a.chunk, lo = tid * c, hi = lo + c;
@@ -286,6 +290,11 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     }
   }
   if (a.offs_smem && tid == 0) soffs[NC] = uint32_t(a.offs[min(n, gbase + NC)]);
+  if (PT == 512 && a.slice_smem)  // removal reads its row slices without a global round trip
+    for (uint32_t v = tid; v < n; v += PT) {
+      const uint32_t* sg = a.seg + size_t(v) * (CS + 1) + rank;
+      sslice[v] = sg[0] | (sg[1] << 16);
+    }
   for (uint32_t e = tid; e < NW * NW; e += PT) {
     const uint32_t b = e / NW + 1, ww = e % NW;
     const uint32_t jj = ww % b;
@@ -300,6 +309,20 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   }
   cl.sync();  // every CTA's mbarriers exist before the first push
 
+  // CTA `rank`'s slice [s0, s1) of row v (offsets inside the row)
+  // (512-thread CTAs only: the cores large enough for 1024-thread CTAs never
+  // fit every row's slices, and their 64-register budget has no room)
+  auto slice_of = [&](uint32_t v, uint32_t& s0, uint32_t& s1) {
+    if (PT == 512 && a.slice_smem) {
+      const uint32_t x = sslice[v];
+      s0 = x & 0xffffu;
+      s1 = x >> 16;
+    } else {
+      const uint32_t* sg = a.seg + size_t(v) * (CS + 1) + rank;
+      s0 = sg[0];
+      s1 = sg[1];
+    }
+  };
   uint32_t removed = 0, pos = 0, useB = 0;  // useB bit k: phase parity of mbB[k]
   bool marked = false;  // my chunk holds BATCH marks of the previous batch
   unsigned long long nbat = 0, nsimple = 0, nlarge = 0, clarge = 0, mlarge = 0;
@@ -434,9 +457,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         const uint32_t vj = __shfl_sync(~0u, rfirst, lj);
         uint32_t dj = __shfl_sync(~0u, rdeg, lj);
         uint64_t oj = __shfl_sync(~0u, rr0, lj);
-        if (dj >= kSliceMin) {  // long row: only this CTA's slice (one more L2 round trip)
-          const uint32_t* sg = a.seg + size_t(vj) * (CS + 1) + rank;
-          const uint32_t s0 = sg[0], s1 = sg[1];
+        if (dj >= kSliceMin) {  // long row: only this CTA's slice
+          uint32_t s0, s1;
+          slice_of(vj, s0, s1);
           oj += s0;
           dj = s1 - s0;
         }
@@ -511,8 +534,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           const uint32_t j = wm3 & 0xffu;
           const Member& mj = s.stage[par][j];
           // only this CTA's slice of the member's row
-          const uint32_t* sg = a.seg + size_t(mj.v) * (CS + 1) + rank;
-          const uint32_t s0 = sg[0], s1 = sg[1];
+          uint32_t s0, s1;
+          slice_of(mj.v, s0, s1);
           remove_local<false, UQ>(adj4, keys_s,
                                   (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, s1 - s0,
                                   mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NC,
@@ -522,9 +545,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           uint32_t s0 = 0, s1 = 0;
           if (lane < bs) {
             mj = s.stage[par][lane];
-            const uint32_t* sg = a.seg + size_t(mj.v) * (CS + 1) + rank;
-            s0 = sg[0];
-            s1 = sg[1];
+            slice_of(mj.v, s0, s1);
           }
           remove_flat<PT>(adj4, keys_s, bs, mj.v, s1 - s0,
                           (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, w, lane, gbase, NC,
@@ -539,8 +560,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         for (uint32_t j = w; j < bs; j += NW) {
           const uint32_t vj = a.perm[pos + j];
           const uint64_t oj = a.offs[vj];
-          const uint32_t* sg = a.seg + size_t(vj) * (CS + 1) + rank;
-          const uint32_t s0 = sg[0], s1 = sg[1];
+          uint32_t s0, s1;
+          slice_of(vj, s0, s1);
           remove_local<false, UQ>(adj4, keys_s, oj + s0, s1 - s0, vj, 0, 1, lane, gbase, NC,
                                   reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
         }
@@ -574,9 +595,10 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   cl.sync();  // no CTA exits while a push into it could be in flight
 }
 
-inline size_t smem_bytes(uint32_t sh, bool offs_smem) {
+inline size_t smem_bytes(uint32_t sh, bool offs_smem, uint64_t slice_n = 0) {
   const size_t NC = size_t(1) << sh;
-  return ((NC * 4 * (offs_smem ? 2 : 1) + 4 + 15) & ~size_t(15)) + sizeof(Fixed);
+  return ((NC * 4 * (offs_smem ? 2 : 1) + 4 + 15) & ~size_t(15)) +
+         ((slice_n * 4 + 15) & ~size_t(15)) + sizeof(Fixed);
 }
 
 }  // namespace peelc
