@@ -40,6 +40,10 @@ constexpr int KC_THREADS = 1024;
 constexpr uint32_t CH = 32;     // arcs per chunk = one warp step
 constexpr int UC = 2;           // chunks in flight per warp (short-row steps)
 constexpr int SC = 8;           // chunks per super-chunk (one warp step on long rows)
+#ifndef DG_KC_HUBS
+#define DG_KC_HUBS 16384        // big rounds: decrements of ids below this summed per CTA
+#endif
+constexpr uint32_t HUBS = DG_KC_HUBS;
 constexpr uint32_t BUF = 8192;  // per-CTA crossing buffer
 constexpr uint32_t kUnset = 0xffffffffu;
 constexpr uint64_t M36 = (1ULL << 36) - 1;
@@ -82,6 +86,7 @@ struct KcArgs {
 };
 
 struct Smem {
+  uint32_t hub[HUBS > 0 ? HUBS : 1];  // per-CTA decrement sums of low ids (big rounds)
   uint32_t id[BUF];  // staged vertices (next frontier / level-advance candidates)
   uint32_t rd[BUF];  // residual degree of a level-advance candidate
   uint64_t tileA[KC_THREADS];
@@ -291,7 +296,7 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t x, uint32_t src) {
 // K loads in flight before any atomic; a decrement that lands the degree
 // on the bound enrols the vertex in the next frontier (warp-aggregated slot
 // in the CTA's crossing buffer).
-template <bool BM, int K>
+template <bool BM, int K, bool HUB = false>
 __device__ __forceinline__ void expand_targets(const KcArgs& a, const uint32_t (&u)[K],
                                                uint32_t b32, Smem& s, Acc* nacc) {
   bool live[K];
@@ -300,6 +305,10 @@ __device__ __forceinline__ void expand_targets(const KcArgs& a, const uint32_t (
     const uint32_t uv = u[k];
     live[k] = false;
     if (uv == kUnset) continue;
+    if (HUB && uv < HUBS) {  // summed in shared memory, applied once per CTA (hub_flush)
+      atomicAdd(&s.hub[uv], 1u);
+      continue;
+    }
     if (BM)
       live[k] = ((ld_relaxed_u32(&a.alive[uv >> 5]) >> (uv & 31)) & 1u) != 0;  // removed?
     else
@@ -405,6 +414,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
   const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
 
+  for (uint32_t h = threadIdx.x; h < HUBS; h += blockDim.x) s.hub[h] = 0;
   uint32_t f = 0;       // frontier generation
   uint32_t lv = 0;      // live buffer holding the current live list
   uint32_t livec = a.n;
@@ -557,15 +567,16 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     }
     if (threadIdx.x == 0) s.cnt = 0;
     __syncthreads();
+    const uint32_t b32r = uint32_t(bound);
+    // big rounds: one super-chunk = SC consecutive 32-arc chunks of the
+    // frontier's virtual arc space per warp step; rounds too small to give
+    // every warp two super-chunks keep one 32-arc chunk per step (UC in
+    // flight), so their work spreads over the whole grid
+    const bool wide = (Ftot + CH - 1) / CH >= uint64_t(nwarps) * SC * 2;
     {
       const Frontier& F = a.fr[f & 1];
       const uint32_t b32 = uint32_t(bound);
       const uint64_t nch = (Ftot + CH - 1) / CH;
-      // big rounds: one super-chunk = SC consecutive 32-arc chunks of the
-      // frontier's virtual arc space per warp step; rounds too small to give
-      // every warp two super-chunks keep one 32-arc chunk per step (UC in
-      // flight), so their work spreads over the whole grid
-      const bool wide = nch >= uint64_t(nwarps) * SC * 2;
       const uint64_t nsc = wide ? (nch + SC - 1) / SC : 0;
       if (!wide)
         for (uint64_t cb = gwarp; cb < nch; cb += nwarps * UC) {
@@ -605,18 +616,49 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
             const uint64_t p = shfl64(fo, l) + (x - shfl64(fa, l));
             u[k] = x < Ftot ? a.adj[p] : kUnset;
           }
-          expand_targets<BM, SC>(a, u, b32, s, nacc);
+          expand_targets<BM, SC, (HUBS > 0)>(a, u, b32, s, nacc);
         } else {
           // many short rows: one 32-arc chunk per step, UC in flight
           for (uint64_t cb = c0; cb <= clast; cb += UC) {
             uint32_t u[UC];
             load_chunks<UC>(F, a.adj, cb, 1, clast + 1, Fc, Ftot, lane, u, nch);
-            expand_targets<BM, UC>(a, u, b32, s, nacc);
+            expand_targets<BM, UC, (HUBS > 0)>(a, u, b32, s, nacc);
           }
         }
       }
     }
     __syncthreads();
+    if (HUBS > 0 && wide) {
+      // big round: every CTA applies its summed decrements of the low ids
+      // (RMAT's hubs) with one atomic each; the sum that takes the degree
+      // from above the bound to at/below it enrols the vertex
+      for (uint32_t h0 = 0; h0 < HUBS; h0 += blockDim.x) {
+        const uint32_t h = h0 + threadIdx.x;
+        const uint32_t c = h < HUBS ? s.hub[h] : 0u;
+        bool cross = false;
+        if (c) {
+          s.hub[h] = 0;
+          const bool alive = BM ? ((ld_relaxed_u32(&a.alive[h >> 5]) >> (h & 31)) & 1u) != 0
+                                : a.labels[h] == kUnset;
+          if (alive) {
+            const uint32_t old = atomicSub(&a.deg[h], c);
+            cross = old > b32r && old - c <= b32r;
+          }
+        }
+        const uint32_t cm = __ballot_sync(~0u, cross);
+        if (cm) {
+          uint32_t base = 0;
+          if (lane == __ffs(cm) - 1) base = atomicAdd(&s.cnt, uint32_t(__popc(cm)));
+          base = __shfl_sync(~0u, base, __ffs(cm) - 1);
+          if (cross) {
+            const uint32_t slot = base + __popc(cm & ((1u << lane) - 1u));
+            if (slot < BUF) s.id[slot] = h;
+            else nacc->ovf = 1;
+          }
+        }
+      }
+      __syncthreads();
+    }
     if (PROF && P && rounds <= 4096) {
       a.rtrace[3 * (rounds - 1)] = clock64() - tp;
       a.rtrace[3 * (rounds - 1) + 1] = Fc;
