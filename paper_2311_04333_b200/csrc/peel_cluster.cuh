@@ -327,8 +327,17 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   bool marked = false;  // my chunk holds BATCH marks of the previous batch
   unsigned long long nbat = 0, nsimple = 0, nlarge = 0, clarge = 0, mlarge = 0;
   const bool P = DG_PEEL_PROF && rank == 0 && tid == 0;
+  // DG_PEEL_PROF timeline: every CTA's thread 0 stamps (SM clock) batches
+  // [arm - 1, arm + 7) into prof[16 + ((batch * 16) + rank) * 8 + k]:
+  // k = 0 loop top, 1 summary pushed, 2 summaries arrived, 3 removal done, 4 end
+  const unsigned long long arm = (DG_PEEL_PROF && a.prof) ? a.prof[15] : 0ULL;
+  auto stamp = [&](unsigned long long b, int k) {
+    if (DG_PEEL_PROF && tid == 0 && arm && b + 1 >= arm && b + 1 < arm + 8)
+      a.prof[16 + ((b + 1 - arm) * 16 + rank) * 8 + k] = clock64();
+  };
   long long c1 = 0, c2 = 0, c3 = 0, tm = DG_PEEL_PROF ? clock64() : 0;
   while (removed < n) {
+    stamp(nbat, 0);
     const uint32_t par = uint32_t(nbat & 1);
     const uint32_t mbA = smem_u32(&s.mbA[par]), mbB = smem_u32(&s.mbB[par]);
     // ---- retire my BATCH marks (no decrement of this CTA's keys runs
@@ -407,7 +416,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         st_async(dst + 16, make_uint4(uint32_t(r0), uint32_t(r0 >> 32), 0u, 0u), bar);
       }
     }
+    stamp(nbat, 1);
     mbar_wait(mbA, uint32_t(nbat >> 1) & 1u);
+    stamp(nbat, 2);
     if (P) {
       const long long t = clock64();
       c1 += t - tm;
@@ -479,6 +490,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         c2 += t - tm;
         tm = t;
       }
+      stamp(nbat, 3);
       __syncthreads();
     } else {
       // ---- general batch (bs >= 2): owners write the batch in ascending id
@@ -574,6 +586,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       c3 += t - tm;
       tm = t;
     }
+    stamp(nbat, 4);
     pos += bs;
     removed += bs;
     ++nbat;
