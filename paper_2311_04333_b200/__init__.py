@@ -560,6 +560,18 @@ def flush_l2() -> None:
     _chk(LIB.dg_flush_l2())
 
 
+_DIAG = None
+
+
+def diag():
+    """The diagnostics library (microbenchmarks, profiling read-outs; tools only)."""
+    global _DIAG
+    if _DIAG is None:
+        from ._abi import load_diag
+        _DIAG = load_diag()
+    return _DIAG
+
+
 def trim_memory() -> None:
     """Return the library's cached device memory to the driver (dg_trim_memory)."""
     _chk(LIB.dg_trim_memory())

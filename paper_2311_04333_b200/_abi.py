@@ -131,13 +131,29 @@ PROTOTYPES = {
     "dg_launch_count": (C.c_uint64, []),
     "dg_flush_l2": (C.c_int, []),
     "dg_trim_memory": (C.c_int, []),
+    "dg_set_peel_mode": (C.c_int, [C.c_int]),
+}
+
+
+DIAG_PATH = os.path.join(PKG, "libdg_b200_diag.so")
+DIAG_PROTOTYPES = {
     "dg_microbench": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_double)]),
     "dg_peel_profile": (C.c_int, [u64p]),
     "dg_peel_trace_arm": (C.c_int, [C.c_uint32]),
     "dg_peel_trace_read": (C.c_int, [u64p]),
     "dg_kcore_profile": (C.c_int, [u64p]),
-    "dg_set_peel_mode": (C.c_int, [C.c_int]),
 }
+
+
+def load_diag(path: str = "") -> C.CDLL:
+    """The diagnostics library (include/dg_b200_diag.h) built against the
+    loaded product library (DG_B200_LIB selects a tuning build): tools only."""
+    path = path or os.environ.get("DG_B200_LIB", LIB_PATH)[:-3] + "_diag.so"
+    lib = C.CDLL(path)
+    for name, (res, args) in DIAG_PROTOTYPES.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:

@@ -21,13 +21,20 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
+DIAG_SRC = os.path.join(CSRC, "microbench.cu")
+DIAG_LIB = os.path.join(PKG, "libdg_b200_diag.so")
+
+
 def _sources():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+    """The product library's sources (diagnostics build separately)."""
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith(".cu") and os.path.join(CSRC, f) != DIAG_SRC)
 
 
 def _headers():
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    return hs + [os.path.join(ROOT, "include", "dg_b200.h")]
+    return hs + [os.path.join(ROOT, "include", "dg_b200.h"),
+                 os.path.join(ROOT, "include", "dg_b200_diag.h")]
 
 
 def _compile(src: str, verbose: bool, extra=(), obj_dir: str = OBJ) -> str:
@@ -66,7 +73,26 @@ def build(verbose: bool = True, extra=(), tag: str = "") -> str:
             print(f"[build] linked {lib}", flush=True)
     if not tag:
         build_cli(lib, verbose)
+    build_diag(lib, obj_dir, verbose)
     return lib
+
+
+def build_diag(lib: str, obj_dir: str = OBJ, verbose: bool = True) -> str:
+    """<lib>_diag.so: latency microbenchmarks and profiling read-outs
+    (include/dg_b200_diag.h), linked against the library `lib` (the product
+    library, or a tuning build of it)."""
+    obj = _compile(DIAG_SRC, verbose, (), obj_dir)
+    diag = lib[:-3] + "_diag.so"
+    if not os.path.exists(diag) or os.path.getmtime(diag) < max(os.path.getmtime(obj),
+                                                               os.path.getmtime(lib)):
+        cmd = [NVCC, *ARCH, "-shared", "-o", diag, obj, lib,
+               "-Xlinker", "-rpath,$ORIGIN", "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"diag link failed:\n{r.stderr[-4000:]}")
+        if verbose:
+            print(f"[build] linked {diag}", flush=True)
+    return diag
 
 
 CLI_SRC = os.path.join(PKG, "cli", "densest.cpp")

@@ -7,6 +7,10 @@
 
 #include "common.cuh"
 
+#ifndef DG_KCORE_PROFILE_WORDS
+#define DG_KCORE_PROFILE_WORDS (8 + 6 * 4096)  // mirrors include/dg_b200_diag.h
+#endif
+
 // Device-resident CSR (reference Graph, graph.hpp:24-45): offs u64[n+1],
 // adj u32[2m] (rows ascending), orig u64[n] (dense id -> original id).
 struct dg_graph {

@@ -6,6 +6,7 @@
 #include <cooperative_groups.h>
 
 #include "internal.cuh"
+#include "dg_b200_diag.h"
 
 namespace cg = cooperative_groups;
 

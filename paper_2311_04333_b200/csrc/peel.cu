@@ -511,6 +511,9 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
   // core 2.98 vs 3.20), the candidate-list kernel when no cluster fits
   const int mode = g_peel_mode.load(std::memory_order_relaxed);
   if (k32 && !one_at_a_time && mode == 0 && g.n > kQueueMinN) {
+    // DG_CLUSTER_CS=8 prefers the 8-CTA cluster (tuning)
+    static const bool pref8 = getenv("DG_CLUSTER_CS") && atoi(getenv("DG_CLUSTER_CS")) == 8;
+    if (pref8 && launch_cluster<8>(g, d_loads, base, false, d_perm, d_raw, d_batches)) return;
     if (launch_cluster<16>(g, d_loads, base, false, d_perm, d_raw, d_batches)) return;
     if (launch_cluster<8>(g, d_loads, base, false, d_perm, d_raw, d_batches)) return;
   }

@@ -14,8 +14,12 @@ HEADER = os.path.join(ROOT, "include", "dg_b200.h")
 LIB = os.path.join(ROOT, "paper_2311_04333_b200", "libdg_b200.so")
 
 
-def declared_symbols():
-    src = open(HEADER).read()
+DIAG_HEADER = os.path.join(ROOT, "include", "dg_b200_diag.h")
+DIAG_LIB = os.path.join(ROOT, "paper_2311_04333_b200", "libdg_b200_diag.so")
+
+
+def declared_symbols(header=HEADER):
+    src = open(header).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(dg_[a-z0-9_]+)\s*\(", src)))
 
@@ -27,6 +31,19 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 20
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
+
+
+def test_diagnostics_live_in_their_own_library():
+    """Latency microbenchmarks and profiling read-outs are not in the product
+    library: include/dg_b200_diag.h <-> libdg_b200_diag.so only."""
+    from paper_2311_04333_b200 import _abi
+    diag = declared_symbols(DIAG_HEADER)
+    assert diag and not set(diag) & set(declared_symbols())
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    assert not set(diag) & set(re.findall(r"\b(dg_[a-z0-9_]+)\b", out))
+    lib = ctypes.CDLL(DIAG_LIB)
+    assert all(hasattr(lib, x) for x in diag)
+    assert sorted(_abi.DIAG_PROTOTYPES) == diag
 
 
 def test_python_prototypes_match_header():

@@ -19,7 +19,7 @@ for _ in range(2):
         print("run failed after the peel kernel:", e)
 it = r.trace.iters[0] if r else None
 p = np.zeros(16, np.uint64)
-dg.LIB.dg_peel_profile(p.ctypes.data_as(C.POINTER(C.c_uint64)))
+dg.diag().dg_peel_profile(p.ctypes.data_as(C.POINTER(C.c_uint64)))
 b = max(1, int(p[3]))
 if it:
     print(f"core n={it.n} m={it.m} batches={it.batches} order={it.order_ms:.2f} ms "

@@ -19,7 +19,7 @@ for T in Ts:
     r = dg.run(g, dg.RunConfig(iterations=T))
     r = dg.run(g, dg.RunConfig(iterations=T))
     prof = np.zeros(16, np.uint64)
-    dg.LIB.dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
+    dg.diag().dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
     nb = max(1, int(prof[3]))
     it = r.trace.iters[-1]
     print(f"T={T} CS={prof[7]} n={it.n} batches={nb} simple={prof[4]} order={it.order_ms:.3f} ms "

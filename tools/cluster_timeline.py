@@ -16,11 +16,11 @@ T = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 first = int(sys.argv[3]) if len(sys.argv) > 3 else 3000
 g = dg.Graph.generate_rmat(scale, 16 << scale, scale)
 dg.run(g, dg.RunConfig(iterations=T))
-dg.LIB.dg_peel_trace_arm(first)
+dg.diag().dg_peel_trace_arm(first)
 r = dg.run(g, dg.RunConfig(iterations=T))
-dg.LIB.dg_peel_trace_arm(0xFFFFFFFF)
+dg.diag().dg_peel_trace_arm(0xFFFFFFFF)
 buf = np.zeros(8 * 32 * 12, np.uint64)
-dg.LIB.dg_peel_trace_read(buf.ctypes.data_as(C.POINTER(C.c_uint64)))
+dg.diag().dg_peel_trace_read(buf.ctypes.data_as(C.POINTER(C.c_uint64)))
 t = buf[: 8 * 16 * 8].reshape(8, 16, 8).astype(np.int64)
 it = r.trace.iters[-1]
 print(f"scale {scale} T={T}: last iteration n={it.n} batches={it.batches} "

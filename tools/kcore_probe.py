@@ -21,7 +21,7 @@ else:
 for _ in range(2):
     r = dg.run(g, dg.RunConfig(iterations=1))
 p = np.zeros(8 + 6 * 4096, np.uint64)
-dg.LIB.dg_kcore_profile(p.ctypes.data_as(C.POINTER(C.c_uint64)))
+dg.diag().dg_kcore_profile(p.ctypes.data_as(C.POINTER(C.c_uint64)))
 ghz = 1.965e3
 names = ["lvl_min", "lvl_sync", "collect", "expand", "flush", "exp_sync"]
 print(f"n={g.n} m={g.m} rounds={r.trace.init.peel_rounds} kmax={r.trace.init.kmax} "

@@ -19,10 +19,10 @@ ITERS = [20000, 20000, 100000, 1000000, 200000, 20000, 20000, 200000, 100000, 10
 out = {}
 for i, (name, it) in enumerate(zip(NAMES, ITERS)):
     ns = C.c_double()
-    st = dg.LIB.dg_microbench(i, it, C.byref(ns))
+    st = dg.diag().dg_microbench(i, it, C.byref(ns))
     out[name] = round(ns.value, 2) if st == 0 else f"error {st}: {dg.LIB.dg_last_error().decode()}"
 for i, name in zip(range(11, 19), NAMES[11:19]):  # the same in SM cycles
     v = C.c_double()
-    if dg.LIB.dg_microbench(100 + i, ITERS[i], C.byref(v)) == 0:
+    if dg.diag().dg_microbench(100 + i, ITERS[i], C.byref(v)) == 0:
         out[name.replace("_ns", "_cycles")] = round(v.value, 2)
 print(json.dumps(out))

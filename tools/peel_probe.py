@@ -25,11 +25,11 @@ for it in r.trace.iters:
           f"arcs/batch={2 * it.m / max(1, it.batches):8.0f}")
 
 # instrumented rerun of the last iteration's core (cycle split; timeline window unreachable)
-dg._chk(dg.LIB.dg_peel_trace_arm(0xFFFFFFF0))
+dg._chk(dg.diag().dg_peel_trace_arm(0xFFFFFFF0))
 dg.run(g, dg.RunConfig(iterations=T))
-dg._chk(dg.LIB.dg_peel_trace_arm(0xFFFFFFFF))
+dg._chk(dg.diag().dg_peel_trace_arm(0xFFFFFFFF))
 prof = np.zeros(16, np.uint64)
-dg.LIB.dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
+dg.diag().dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
 tot = max(1, int(prof[:3].sum()))
 print(f"last peel launch: batches={prof[3]} cycles/batch S1={prof[0]/max(1,prof[3]):.0f} "
       f"S2={prof[1]/max(1,prof[3]):.0f} S3={prof[2]/max(1,prof[3]):.0f} "
@@ -41,7 +41,7 @@ if len(sys.argv) > 3:  # also time iteration 1's core with the other kernel mode
     dg.set_peel_mode(mode)
     r = dg.run(g, dg.RunConfig(iterations=2))
     it = r.trace.iters[0]
-    dg.LIB.dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
+    dg.diag().dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
     print(f"mode {mode}: it1 n={it.n} batches={it.batches} order={it.order_ms:.3f}ms "
           f"us/batch={1e3 * it.order_ms / max(1, it.batches):.2f}")
     print(f"  last launch (it2) cycles/batch S1={prof[0]/max(1,prof[3]):.0f} "

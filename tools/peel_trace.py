@@ -23,12 +23,12 @@ g = dg.Graph.from_pairs(u, v)
 del u, v
 mode = int(sys.argv[3], 0) if len(sys.argv) > 3 else 0
 dg.set_peel_mode(mode)
-dg._chk(dg.LIB.dg_peel_trace_arm(first))
+dg._chk(dg.diag().dg_peel_trace_arm(first))
 T = int(os.environ.get("DG_TRACE_T", "3"))  # 1: iteration 1's core
 r = dg.run(g, dg.RunConfig(iterations=T))
 tr = np.zeros(8 * 32 * 12, np.uint64)
-dg._chk(dg.LIB.dg_peel_trace_read(tr.ctypes.data_as(C.POINTER(C.c_uint64))))
-dg._chk(dg.LIB.dg_peel_trace_arm(0xFFFFFFFF))  # disarm
+dg._chk(dg.diag().dg_peel_trace_read(tr.ctypes.data_as(C.POINTER(C.c_uint64))))
+dg._chk(dg.diag().dg_peel_trace_arm(0xFFFFFFFF))  # disarm
 tr = tr.reshape(8, 32, 12).astype(np.int64)
 print(f"core n={r.trace.iters[-1].n} batches={r.trace.iters[-1].batches}")
 hdr = ("batch  top->A(last w)  A wait  S2(last w)  B wait  S3(last w)  C wait | total")

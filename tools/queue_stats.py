@@ -8,5 +8,5 @@ g = dg.Graph.from_pairs(u, v)
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 r = dg.run(g, dg.RunConfig(iterations=T))
 prof = np.zeros(16, np.uint64)
-dg.LIB.dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
+dg.diag().dg_peel_profile(prof.ctypes.data_as(C.POINTER(C.c_uint64)))
 print("batches", prof[3], "rebases", prof[9], "full-scan batches", prof[10], "list batches", prof[11])
