@@ -381,10 +381,10 @@ KeyRange key_range(const dg_graph& g, const uint64_t* d_loads) {
 }
 
 // Per-row CTA slices for the cluster kernel: seg[v*(CS+1) + r] = index
-// inside row v of its first neighbour >= r << sh (rows ascend), one thread
+// inside row v of its first neighbour >= r * nc (rows ascend), one thread
 // per (row, r) by binary search.
 template <int CS>
-__global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t n, uint32_t sh,
+__global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t n, uint32_t nc,
                             uint32_t* seg) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * (CS + 1);
        i += uint64_t(gridDim.x) * blockDim.x) {
@@ -395,7 +395,7 @@ __global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t 
     if (r == 0) {
       hi = 0;
     } else if (r < CS) {
-      const uint32_t x = r << sh;
+      const uint32_t x = r * nc;
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (adj[o0 + mid] < x) lo = mid + 1; else hi = mid;
@@ -408,17 +408,17 @@ __global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t 
 // Cluster variant: returns false when no cluster configuration fits.
 template <int CS, int PT>
 bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
-                       uint32_t sh, uint32_t* d_perm, uint64_t* d_raw,
+                       uint32_t nc, uint32_t* d_perm, uint64_t* d_raw,
                        unsigned long long* d_batches) {
   const uint64_t n = g.n;
   const bool offs32 = 2 * g.m < 0xffffffffULL;
-  bool offs_smem = offs32 && peelc::smem_bytes(sh, true) <= kSmemCap;
-  if (!offs_smem && peelc::smem_bytes(sh, false) > kSmemCap) return false;
+  bool offs_smem = offs32 && peelc::smem_bytes(nc, true) <= kSmemCap;
+  if (!offs_smem && peelc::smem_bytes(nc, false) > kSmemCap) return false;
   // every row's slice bounds in shared memory when they fit (rows < 2^16 arcs)
   const bool slice_smem = PT == 512 && g.maxdeg < 65536 &&
-                          peelc::smem_bytes(sh, offs_smem, n) <= kSmemCap &&
+                          peelc::smem_bytes(nc, offs_smem, n) <= kSmemCap &&
                           !getenv("DG_NO_SLICE_SMEM");
-  const size_t smem = peelc::smem_bytes(sh, offs_smem, slice_smem ? n : 0);
+  const size_t smem = peelc::smem_bytes(nc, offs_smem, slice_smem ? n : 0);
   auto kern = peelc::k_peel_cluster<CS, PT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess) {
@@ -452,10 +452,10 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
   DG_CUDA(cudaMemsetAsync(d_raw, 0, n * sizeof(uint64_t), stream()));
   DevBuf<uint32_t> seg(n * (CS + 1));
   k_seg_table<CS><<<grid_for(n * (CS + 1), 256), 256, 0, stream()>>>(g.offs.get(), g.adj.get(), n,
-                                                                      sh, seg.get());
+                                                                      nc, seg.get());
   DG_CHECK_LAUNCH();
   peelc::Args a{g.offs.get(), g.adj.get(), uint32_t(n), d_loads, base, one ? 1 : 0,
-                sh, (1u << sh) / PT, offs_smem ? 1 : 0, d_perm, d_raw, seg.get(),
+                nc, nc / PT, offs_smem ? 1 : 0, d_perm, d_raw, seg.get(),
                 slice_smem ? 1 : 0, d_batches, peel_prof_buffer()};
   DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   count_launch();
@@ -469,17 +469,24 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
 template <int CS>
 bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
                     uint32_t* d_perm, uint64_t* d_raw, unsigned long long* d_batches) {
-  uint32_t sh = 9;  // NC = 2^sh ids per CTA
-  while ((uint64_t(CS) << sh) < g.n) ++sh;
-  int pt = sh <= 12 ? 512 : 1024;
+  // NC ids per CTA: the smallest multiple of the CTA size covering n / CS, so
+  // every CTA of the cluster holds vertices (power-of-two blocks left 7 of 16
+  // CTAs empty on RMAT-26's 17.9K core); DG_CLUSTER_POW2=1 restores them.
+  const uint64_t per_cta = (g.n + CS - 1) / CS;
+  int pt = per_cta <= 4096 ? 512 : 1024;
   if (const char* e = getenv("DG_CLUSTER_PT")) pt = atoi(e) == 512 ? 512 : 1024;
-  if (pt == 1024) sh = sh < 10 ? 10 : sh;
-  // <= 32 keys per thread (the S1 match mask)
-  if (pt == 512 && sh <= 14)
-    return launch_cluster_pt<CS, 512>(g, d_loads, base, one, sh, d_perm, d_raw, d_batches);
-  if (sh <= 15)
-    return launch_cluster_pt<CS, 1024>(g, d_loads, base, one, sh, d_perm, d_raw, d_batches);
-  return false;
+  uint64_t c = (per_cta + pt - 1) / pt;  // keys per thread
+  if (getenv("DG_CLUSTER_POW2") && getenv("DG_CLUSTER_POW2")[0] == '1') {
+    uint64_t nc = 512;
+    while (nc * CS < g.n) nc *= 2;
+    if (nc < uint64_t(pt)) nc = pt;
+    c = nc / pt;
+  }
+  if (c > 32) return false;  // <= 32 keys per thread (the S1 match mask)
+  const uint32_t nc = uint32_t(c * pt);
+  if (pt == 512)
+    return launch_cluster_pt<CS, 512>(g, d_loads, base, one, nc, d_perm, d_raw, d_batches);
+  return launch_cluster_pt<CS, 1024>(g, d_loads, base, one, nc, d_perm, d_raw, d_batches);
 }
 
 void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
