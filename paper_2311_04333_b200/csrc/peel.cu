@@ -462,10 +462,7 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
   return true;
 }
 
-// CTA size by block size: 512 threads while a CTA owns at most 4K ids
-// (RMAT-22's 35K core: 4.18 vs 4.37 us per batch), 1024 beyond (RMAT-26's
-// 84K core: 16 ids per thread at 512 make the scan the bottleneck).
-// DG_CLUSTER_PT=512|1024 overrides (tuning).
+// CTA size by block size (see below); DG_CLUSTER_PT=512|1024 overrides (tuning).
 template <int CS>
 bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
                     uint32_t* d_perm, uint64_t* d_raw, unsigned long long* d_batches) {
@@ -473,7 +470,9 @@ bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, b
   // every CTA of the cluster holds vertices (power-of-two blocks left 7 of 16
   // CTAs empty on RMAT-26's 17.9K core); DG_CLUSTER_POW2=1 restores them.
   const uint64_t per_cta = (g.n + CS - 1) / CS;
-  int pt = per_cta <= 4096 ? 512 : 1024;
+  // 512-thread CTAs up to 12 keys per thread (RMAT-26's 84K core: 3.72 vs
+  // 3.78 us/batch at 1024), 1024 beyond
+  int pt = per_cta <= 6144 ? 512 : 1024;
   if (const char* e = getenv("DG_CLUSTER_PT")) pt = atoi(e) == 512 ? 512 : 1024;
   uint64_t c = (per_cta + pt - 1) / pt;  // keys per thread
   if (getenv("DG_CLUSTER_POW2") && getenv("DG_CLUSTER_POW2")[0] == '1') {
