@@ -37,14 +37,26 @@ namespace dgb {
 namespace {
 
 constexpr int KC_THREADS = 1024;
+#ifndef DG_KC_COLD
+#define DG_KC_COLD __forceinline__
+#endif
 constexpr uint32_t CH = 32;     // arcs per chunk = one warp step
 constexpr int UC = 2;           // chunks in flight per warp (short-row steps)
 constexpr int SC = 8;           // chunks per super-chunk (one warp step on long rows)
 #ifndef DG_KC_HUBS
-#define DG_KC_HUBS 16384        // big rounds: decrements of ids below this summed per CTA
+#define DG_KC_HUBS 8192         // big rounds: decrements of ids below this summed per CTA
 #endif
 constexpr uint32_t HUBS = DG_KC_HUBS;
-constexpr uint32_t BUF = 8192;  // per-CTA crossing buffer
+#ifndef DG_KC_BUF
+#define DG_KC_BUF 8192
+#endif
+constexpr uint32_t BUF = DG_KC_BUF;  // per-CTA crossing buffer
+#ifndef DG_KC_LB
+#define DG_KC_LB 4096
+#endif
+constexpr uint32_t LB = DG_KC_LB;  // per-CTA buffer of low-list entries (degree crossing theta)
+constexpr uint32_t NB = 1024;   // degree histogram bins of a full level pass (= KC_THREADS)
+constexpr uint32_t HS = 32;     // histogram sampling stride (one lane per warp step)
 constexpr uint32_t kUnset = 0xffffffffu;
 constexpr uint64_t M36 = (1ULL << 36) - 1;
 
@@ -68,7 +80,7 @@ struct KcArgs {
   const uint64_t* offs;
   const uint32_t* adj;
   uint32_t n;
-  uint32_t* deg;
+  uint32_t* deg;  // residual degrees
   uint32_t* labels;
   uint32_t* live0;
   uint32_t* live1;
@@ -76,12 +88,18 @@ struct KcArgs {
   uint32_t* alive;  // alive bitmap (n bits; large graphs only, see k_coreness<BM>)
   Frontier fr[2];
   Acc* acc;  // [3]
+  // low list (exact mode): every alive vertex with degree < theta, so level
+  // advances scan it instead of the whole live list (see k_coreness)
+  uint32_t* low[2];
+  unsigned long long* lt;  // [2] entries in low[0] / low[1]
+  uint32_t* hist;          // [NB] sampled degree histogram of a full pass (zero between uses)
   GridBarrier* bar;
   uint32_t* out;               // kmax, rounds, err
   unsigned long long* rtrace;  // [3*4096] per-round expand cycles, Fc, Ftot, then
                                // [3*4096] per-level-pass cycles, live entries, spilled (diagnostic)
   unsigned long long* prof;    // [8] block-0 cycles (see dg_kcore_profile)
   int approx;
+  int nolow;  // DG_KCORE_LOWLIST=0: no low list (every level advance a full pass)
   uint64_t c_num, c_den;
 };
 
@@ -92,8 +110,15 @@ struct Smem {
   uint64_t tileA[KC_THREADS];
   uint64_t ws[33];
   uint32_t ws32[33];
+  uint32_t hst[NB];  // sampled degree histogram of a full level pass
+  uint32_t lid[LB];  // staged low-list entries (degree crossed theta this round)
   uint32_t cnt;
+  uint32_t lcnt;
   uint32_t cmin;  // running CTA minimum of a level pass (exact mode)
+  uint32_t tbin;  // scratch: histogram bin that sets theta
+  uint32_t kth;   // theta (low-list threshold, 0 = no low list)
+  uint32_t klb;   // low-list buffer being extended
+  unsigned long long b_lc;
   unsigned long long baseF, baseL;
   // phase scalars fetched by thread 0 after each grid barrier
   uint32_t abort;
@@ -106,6 +131,9 @@ struct Smem {
 // global list), so the usual small jump needs no second pass.
 constexpr uint32_t LW = 16;
 constexpr int LE = 4;  // live-list entries per thread in the level pass
+constexpr uint32_t LFRAC = 8;  // low list ~ 1/LFRAC of the alive vertices at a rebuild
+constexpr uint32_t LMIN = 8;   // ... and at least LMIN degree values past the bound
+static_assert(NB == KC_THREADS, "one histogram bin per thread");
 
 __device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
   s.b_front = ld_relaxed_u64(&acc->front);
@@ -114,6 +142,11 @@ __device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
   s.b_ovf = ld_relaxed_u32(&acc->ovf);
   s.b_live2 = ld_relaxed_u64(&acc->live2);
   s.b_ccnt = ld_relaxed_u64(&acc->ccnt);
+}
+
+// alive bit (BM mode)
+__device__ __forceinline__ bool is_alive(const KcArgs& a, uint32_t v) {
+  return ((ld_relaxed_u32(&a.alive[v >> 5]) >> (v & 31)) & 1u) != 0;
 }
 
 // All threads of the CTA call this with a per-thread candidate (isF, v, d, o).
@@ -162,7 +195,7 @@ __device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d
 // Scan the live list: alive vertices with deg <= bound join the frontier,
 // the other alive ones are compacted into live_out.
 template <bool BM>
-__device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const uint32_t* live_in,
+__device__ DG_KC_COLD void collect(const KcArgs& a, uint32_t livec, bool implicit, const uint32_t* live_in,
                         uint32_t* live_out, uint32_t bound, uint32_t label, const Frontier& F,
                         Acc* acc, Smem& s, unsigned long long* live_ctr) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -173,8 +206,7 @@ __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const ui
     bool isF = false, isL = false;
     if (i < livec) {
       v = implicit ? uint32_t(i) : live_in[i];
-      if (BM ? ((ld_relaxed_u32(&a.alive[v >> 5]) >> (v & 31)) & 1u) != 0
-             : a.labels[v] == kUnset) {
+      if (BM ? is_alive(a, v) : a.labels[v] == kUnset) {
         if (a.deg[v] <= bound) {
           isF = true;
           o = a.offs[v];
@@ -198,18 +230,23 @@ __device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const ui
 // bound staged in shared memory (overflow spilled to a.cand).  E contiguous
 // entries per thread: E independent load chains and one CTA scan per
 // E * blockDim entries.
-template <bool BM, int E>
-__device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint32_t* live_in,
-                                           uint32_t* live_out, uint32_t livec, bool implicit,
-                                           uint64_t win, bool track, Acc* acc, uint32_t& lmin) {
+// hist: also sample the degrees of alive vertices (ids = 0 mod HS) into the
+// CTA's histogram s.hst[min(d - hb, NB - 1)] (full passes of exact mode).
+// LOCAL: the list is this CTA's own (shared memory), not a grid-strided share.
+template <bool BM, int E, bool LOCAL = false>
+__device__ DG_KC_COLD void level_pass(const KcArgs& a, Smem& s, const uint32_t* live_in,
+                                           uint32_t* live_out, uint64_t livec, bool implicit,
+                                           uint64_t win, bool track, Acc* acc,
+                                           unsigned long long* out_ctr, bool hist, uint32_t hb,
+                                           uint32_t& lmin) {
   const uint32_t lane = lane_id();
   const uint64_t tile = uint64_t(blockDim.x) * E;
-  const uint64_t stride = uint64_t(gridDim.x) * tile;
-  for (uint64_t base = uint64_t(blockIdx.x) * tile; base < livec; base += stride) {
+  const uint64_t stride = LOCAL ? tile : uint64_t(gridDim.x) * tile;
+  for (uint64_t base = LOCAL ? 0 : uint64_t(blockIdx.x) * tile; base < livec; base += stride) {
     const uint64_t i0 = base + uint64_t(threadIdx.x) * E;
     uint32_t v[E], d[E];
     bool alive[E];
-    if (E == 4 && !implicit && i0 + E <= livec) {
+    if (E == 4 && !LOCAL && !implicit && i0 + E <= livec) {
       const uint4 q = *reinterpret_cast<const uint4*>(live_in + i0);
       const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -227,9 +264,10 @@ __device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint3
         const uint32_t x = v[e];
         // the degree is read alongside the liveness word (not after it): one
         // dependent round trip per entry instead of two
+        // the degree is read alongside the liveness word (not after it): one
+        // dependent round trip per entry instead of two
         const uint32_t dx = a.deg[x];
-        alive[e] = BM ? ((ld_relaxed_u32(&a.alive[x >> 5]) >> (x & 31)) & 1u) != 0
-                      : a.labels[x] == kUnset;
+        alive[e] = BM ? is_alive(a, x) : a.labels[x] == kUnset;
         if (alive[e]) d[e] = dx;
       }
     }
@@ -238,6 +276,7 @@ __device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint3
     for (int e = 0; e < E; ++e) {
       lmin = min(lmin, d[e]);
       c += alive[e];
+      if (hist && alive[e] && (v[e] & (HS - 1)) == 0) atomicAdd(&s.hst[min(d[e] - hb, NB - 1)], 1u);
       bool spill = false;
       bool near;
       if (track) {
@@ -276,7 +315,7 @@ __device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint3
     }
     uint32_t totL;
     const uint32_t exL = block_excl_scan<uint32_t>(c, s.ws32, &totL);
-    if (threadIdx.x == 0 && totL) s.baseL = atomicAdd(&acc->live, (unsigned long long)totL);
+    if (threadIdx.x == 0 && totL) s.baseL = atomicAdd(out_ctr, (unsigned long long)totL);
     __syncthreads();
     uint64_t o = s.baseL + exL;
 #pragma unroll
@@ -296,9 +335,40 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t x, uint32_t src) {
 // K loads in flight before any atomic; a decrement that lands the degree
 // on the bound enrols the vertex in the next frontier (warp-aggregated slot
 // in the CTA's crossing buffer).
+// A decrement that takes the degree from theta to theta - 1 enrols the vertex
+// in the low list (staged in s.lid, flushed once per CTA at the end of the
+// round; theta = 0 outside exact mode: no alive degree is ever 0 before a
+// decrement).
+#ifdef DG_KC_NOINLINE_LOW
+__device__ __noinline__ void stage_low(
+#else
+__device__ __forceinline__ void stage_low(
+#endif
+bool lx, uint32_t uv, Smem& s, const KcArgs& a,
+                                          const uint32_t& lbs) {
+  const uint32_t lm = __ballot_sync(~0u, lx);
+  if (!lm) return;
+  const uint32_t lane = lane_id();
+  uint32_t base = 0;
+  if (lane == __ffs(lm) - 1) base = atomicAdd(&s.lcnt, uint32_t(__popc(lm)));
+  base = __shfl_sync(~0u, base, __ffs(lm) - 1);
+  const uint32_t slot = base + __popc(lm & ((1u << lane) - 1u));
+  const bool ovf = lx && slot >= LB;
+  if (lx && !ovf) s.lid[slot] = uv;
+  const uint32_t om = __ballot_sync(~0u, ovf);  // CTA buffer full: straight to the list
+  if (om) {
+    unsigned long long gb = 0;
+    const uint32_t lb = lbs;
+    if (lane == __ffs(om) - 1) gb = atomicAdd(&a.lt[lb], (unsigned long long)__popc(om));
+    gb = __shfl_sync(~0u, gb, __ffs(om) - 1);
+    if (ovf) a.low[lb][gb + __popc(om & ((1u << lane) - 1u))] = uv;
+  }
+}
+
 template <bool BM, int K, bool HUB = false>
 __device__ __forceinline__ void expand_targets(const KcArgs& a, const uint32_t (&u)[K],
                                                uint32_t b32, Smem& s, Acc* nacc) {
+  const uint32_t theta = s.kth;
   bool live[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -310,7 +380,7 @@ __device__ __forceinline__ void expand_targets(const KcArgs& a, const uint32_t (
       continue;
     }
     if (BM)
-      live[k] = ((ld_relaxed_u32(&a.alive[uv >> 5]) >> (uv & 31)) & 1u) != 0;  // removed?
+      live[k] = is_alive(a, uv);  // removed?
     else
       live[k] = a.deg[uv] > b32;  // dead, or already at/below the bound
   }
@@ -320,6 +390,13 @@ __device__ __forceinline__ void expand_targets(const KcArgs& a, const uint32_t (
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const bool cross = live[k] && old[k] == b32 + 1;  // crossed: joins the next round
+#ifdef DG_KC_NOSTAGE
+    const bool lx = false;
+#else
+    const bool lx = live[k] && old[k] == theta;       // crossed theta: joins the low list
+#endif
+    if (!__any_sync(~0u, cross || lx)) continue;       // the usual case: one vote
+    stage_low(lx, u[k], s, a, s.klb);
     const uint32_t cm = __ballot_sync(~0u, cross);
     if (!cm) continue;
     uint32_t base = 0;
@@ -415,6 +492,12 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
 
   for (uint32_t h = threadIdx.x; h < HUBS; h += blockDim.x) s.hub[h] = 0;
+  for (uint32_t h = threadIdx.x; h < NB; h += blockDim.x) s.hst[h] = 0;
+  if (threadIdx.x == 0) {
+    s.lcnt = 0;
+    s.kth = 0;
+    s.klb = 0;
+  }
   uint32_t f = 0;       // frontier generation
   uint32_t lv = 0;      // live buffer holding the current live list
   uint32_t livec = a.n;
@@ -425,6 +508,8 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
   uint32_t Fc = 0;
   uint64_t Ftot = 0;
   uint64_t guard = 0;
+  uint32_t lb = 0;          // low list buffer
+  bool hist_dirty = false;  // a.hist holds samples to clear
   const bool P = blockIdx.x == 0 && threadIdx.x == 0;
   long long pr[8] = {}, tp = PROF ? clock64() : 0;
   auto mark = [&](int k) {
@@ -442,43 +527,110 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     }
     if (Fc == 0) {
       if (remaining == 0) break;
-      // ---- level advance: ONE pass over the live list computes the min alive
-      // degree, compacts the list and stages the alive vertices within LW of
-      // the bound; when the new bound lands in that window (the usual case)
-      // the frontier comes from the staged candidates, else a collect pass.
+      // ---- level advance.  Exact mode keeps a LOW LIST: every alive vertex
+      // of degree < theta (built at a full pass, extended by the decrements
+      // that cross theta), so the minimum alive degree -- the next bound,
+      // < theta while the list holds an alive vertex -- comes from a pass
+      // over the low list only; a full pass over the live list (min,
+      // compaction, a sampled degree histogram that sets the next theta,
+      // then the low list rebuilt) runs only when the low list has run dry.
+      // Either pass stages the alive vertices at the running minimum in
+      // shared memory (a CTA's overflow spills to a.cand), so the frontier
+      // usually needs no second pass.  Approximate mode: every level
+      // advance is a full pass staging the vertices within LW of the bound.
       Acc* acc = a.acc + (f % 3);
-      const uint32_t* live_in = lv ? a.live1 : a.live0;
-      uint32_t* live_out = lv ? a.live0 : a.live1;
       const uint64_t win = bound + LW;
       const bool track = !a.approx;
-      if (threadIdx.x == 0) {
-        s.cnt = 0;
-        s.cmin = kUnset;
+      // a low list pays while a full pass takes several tiles per CTA
+      const bool lowok = track && !a.nolow && livec >= 2ULL * gridDim.x * blockDim.x * LE;
+      uint64_t Lc = 0;
+      if (lowok) {
+        if (threadIdx.x == 0) s.b_lc = ld_relaxed_u64(&a.lt[lb]);
+        __syncthreads();
+        Lc = s.b_lc;
       }
-      __syncthreads();
-      uint32_t lmin = kUnset;
-      // wide tiles only while the list fills the grid LE times over
-      if (livec >= uint64_t(gridDim.x) * blockDim.x * LE)
-        level_pass<BM, LE>(a, s, live_in, live_out, livec, implicit, win, track, acc, lmin);
-      else
-        level_pass<BM, 1>(a, s, live_in, live_out, livec, implicit, win, track, acc, lmin);
-      lmin = __reduce_min_sync(~0u, lmin);
-      if (lane == 0) s.ws32[threadIdx.x >> 5] = lmin;
-      __syncthreads();
-      if (threadIdx.x < 32) {
-        uint32_t x = threadIdx.x < (blockDim.x >> 5) ? s.ws32[threadIdx.x] : kUnset;
-        x = __reduce_min_sync(~0u, x);
-        if (threadIdx.x == 0 && x != kUnset) atomicMin(&acc->minv, x);
+      bool full = !lowok || Lc == 0;
+      const uint32_t hb = uint32_t(bound) + 1;  // every alive degree is > bound here
+      for (;;) {
+        if (threadIdx.x == 0) {
+          s.cnt = 0;
+          s.cmin = kUnset;
+        }
+        __syncthreads();
+        uint32_t lmin = kUnset;
+        const uint32_t* in;
+        uint32_t* out;
+        uint64_t cnt;
+        bool imp = false;
+        unsigned long long* octr;
+        if (full) {
+          in = lv ? a.live1 : a.live0;
+          out = lv ? a.live0 : a.live1;
+          cnt = livec;
+          imp = implicit;
+          octr = &acc->live;
+        } else {
+          in = a.low[lb];
+          out = a.low[lb ^ 1];
+          cnt = Lc;
+          octr = &a.lt[lb ^ 1];
+        }
+        const bool hist = full && lowok;
+        // wide tiles only while the list fills the grid LE times over
+        if (cnt >= uint64_t(gridDim.x) * blockDim.x * LE)
+          level_pass<BM, LE>(a, s, in, out, cnt, imp, win, track, acc, octr, hist, hb, lmin);
+        else
+          level_pass<BM, 1>(a, s, in, out, cnt, imp, win, track, acc, octr, hist, hb, lmin);
+        // the low-list entries this CTA staged since the last level advance
+        // (kept in shared memory, no per-round flush) join the pass; a full
+        // pass rebuilds the list, so it drops them
+        if (!full) {
+          level_pass<BM, 1, true>(a, s, s.lid, out, min(s.lcnt, LB), false, win, track, acc, octr,
+                                  false, hb, lmin);
+          if (threadIdx.x == 0) s.lcnt = 0;  // level_pass ended with a CTA barrier
+        } else if (hist && threadIdx.x == 0) {
+          s.lcnt = 0;
+        }
+        lmin = __reduce_min_sync(~0u, lmin);
+        if (lane == 0) s.ws32[threadIdx.x >> 5] = lmin;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          uint32_t x = threadIdx.x < (blockDim.x >> 5) ? s.ws32[threadIdx.x] : kUnset;
+          x = __reduce_min_sync(~0u, x);
+          if (threadIdx.x == 0 && x != kUnset) atomicMin(&acc->minv, x);
+        }
+        if (hist)  // the CTA's samples into the grid histogram (NB == blockDim.x)
+          for (uint32_t i = threadIdx.x; i < NB; i += blockDim.x) {
+            const uint32_t c = s.hst[i];
+            if (c) {
+              s.hst[i] = 0;
+              atomicAdd(&a.hist[i], c);
+            }
+          }
+        if (PROF && P && pr[6] < 4096) {
+          a.rtrace[3 * 4096 + 3 * pr[6]] = clock64() - tp;
+          a.rtrace[3 * 4096 + 3 * pr[6] + 1] = cnt;
+        }
+        mark(0);
+        if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
+        mark(1);
+        if (PROF && P && pr[6] < 4096)
+          a.rtrace[3 * 4096 + 3 * pr[6] + 2] = s.b_ccnt | (full ? (1ULL << 40) : 0ULL);
+        if (PROF && P) ++pr[6];
+        if (full) {
+          livec = uint32_t(s.b_live);
+          lv ^= 1;
+          implicit = false;
+        } else {
+          // every CTA is past the pass over low[lb]: its counter restarts at
+          // 0 for the next compaction into it
+          if (P) a.lt[lb] = 0;
+          lb ^= 1;
+        }
+        if (s.b_minv != kUnset || full) break;
+        full = true;  // the low list held no alive vertex: full pass
       }
-      if (PROF && P && pr[6] < 4096) {
-        a.rtrace[3 * 4096 + 3 * pr[6]] = clock64() - tp;
-        a.rtrace[3 * 4096 + 3 * pr[6] + 1] = livec;
-      }
-      mark(0);
-      if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
-      mark(1);
-      if (PROF && P && pr[6] < 4096) a.rtrace[3 * 4096 + 3 * pr[6] + 2] = s.b_ccnt;
-      if (PROF && P) ++pr[6];
+      if (s.abort) break;
       const uint64_t gmin = s.b_minv;
       if (gmin == kUnset) {  // remaining > 0 but nothing alive: inconsistent
         if (P) a.out[2] = 2;
@@ -496,9 +648,32 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           t = nt;
         }
       }
-      livec = uint32_t(s.b_live);
-      lv ^= 1;
-      implicit = false;
+      const bool rebuild = full && lowok;
+      if (full && !lowok && threadIdx.x == 0) s.kth = 0;  // no low list from here on
+      if (rebuild) {
+        // next theta: the low list should hold about 1/LFRAC of the alive
+        // vertices (sampled histogram of degree - hb), and at least LMIN
+        // degree values beyond the new bound
+        if (threadIdx.x == 0) s.tbin = NB - 1;
+        uint32_t tot;
+        const uint32_t hv = threadIdx.x < NB ? ld_relaxed_u32(&a.hist[threadIdx.x]) : 0u;
+        const uint32_t ex = block_excl_scan<uint32_t>(hv, s.ws32, &tot);
+        const uint32_t target = (tot + LFRAC - 1) / LFRAC;
+        if (threadIdx.x < NB - 1 && hv && ex < target && ex + hv >= target)
+          atomicMin(&s.tbin, threadIdx.x + 1);
+        __syncthreads();
+        uint64_t th = uint64_t(hb) + s.tbin;
+        th = max(th, bound + LMIN);
+        th = min(th, uint64_t(hb) + NB - 1);  // the last bin mixes every larger degree
+        const uint32_t theta = uint32_t(max(th, bound + 1));
+        __syncthreads();  // every thread has read s.tbin
+        if (threadIdx.x == 0) {
+          s.kth = theta;
+          s.klb = lb;
+        }
+        __syncthreads();
+        hist_dirty = true;
+      }
       const Frontier& F0 = a.fr[f & 1];
       if (track || bound <= win) {
         // the frontier = candidates with residual degree <= bound: this CTA's
@@ -529,19 +704,56 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           }
           emit_front_tile(ok, v, dl, o, uint32_t(label), a, F0, acc, s);
         }
+        if (rebuild) {
+          // the low list of the new theta from the compacted live list (into
+          // low[lb], empty here); this round's frontier vertices may enter
+          // too (dead by the next pass, which drops them)
+          // (LE entries per thread, one 16-byte load of the list)
+          const uint32_t* lin = lv ? a.live1 : a.live0;
+          const uint64_t tile = uint64_t(blockDim.x) * LE;
+          for (uint64_t base = uint64_t(blockIdx.x) * tile; base < livec;
+               base += uint64_t(gridDim.x) * tile) {
+            const uint64_t i0 = base + uint64_t(threadIdx.x) * LE;
+            uint32_t v[LE];
+            bool in[LE];
+            if (i0 + LE <= livec) {
+              const uint4 q = *reinterpret_cast<const uint4*>(lin + i0);
+              v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+            } else {
+#pragma unroll
+              for (int e = 0; e < LE; ++e) v[e] = i0 + e < livec ? lin[i0 + e] : 0u;
+            }
+            uint32_t c = 0;
+#pragma unroll
+            for (int e = 0; e < LE; ++e) {
+              in[e] = i0 + e < livec && a.deg[v[e]] < s.kth;
+              c += in[e];
+            }
+            uint32_t tl;
+            const uint32_t el = block_excl_scan<uint32_t>(c, s.ws32, &tl);
+            if (threadIdx.x == 0 && tl) s.baseL = atomicAdd(&a.lt[lb], (unsigned long long)tl);
+            __syncthreads();
+            uint64_t o = s.baseL + el;
+#pragma unroll
+            for (int e = 0; e < LE; ++e)
+              if (in[e]) a.low[lb][o++] = v[e];
+            __syncthreads();
+          }
+        }
         mark(2);
         if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
         mark(1);
       } else {
         // larger jump: collect from the compacted list
-        collect<BM>(a, livec, false, live_out, lv ? a.live0 : a.live1, uint32_t(bound),
-                uint32_t(label), F0, acc, s, &acc->live2);
+        collect<BM>(a, livec, false, lv ? a.live1 : a.live0, lv ? a.live0 : a.live1,
+                    uint32_t(bound), uint32_t(label), F0, acc, s, &acc->live2);
         mark(2);
         if (!grid_sync(a.bar, nb, &s.abort, [&] { fetch_acc(s, acc); })) break;
         mark(1);
         livec = uint32_t(s.b_live2);
         lv ^= 1;
       }
+      if (threadIdx.x == 0) s.klb = lb;
       const unsigned long long pk = s.b_front;
       Fc = uint32_t(pk >> 36);
       Ftot = pk & M36;
@@ -566,6 +778,11 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       r->ccnt = 0;
     }
     if (threadIdx.x == 0) s.cnt = 0;
+    if (hist_dirty) {  // every CTA read the histogram before the last grid barrier
+      if (blockIdx.x == 0)
+        for (uint32_t i = threadIdx.x; i < NB; i += blockDim.x) a.hist[i] = 0;
+      hist_dirty = false;
+    }
     __syncthreads();
     const uint32_t b32r = uint32_t(bound);
     // big rounds: one super-chunk = SC consecutive 32-arc chunks of the
@@ -635,16 +852,17 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       for (uint32_t h0 = 0; h0 < HUBS; h0 += blockDim.x) {
         const uint32_t h = h0 + threadIdx.x;
         const uint32_t c = h < HUBS ? s.hub[h] : 0u;
-        bool cross = false;
+        bool cross = false, lx = false;
         if (c) {
           s.hub[h] = 0;
-          const bool alive = BM ? ((ld_relaxed_u32(&a.alive[h >> 5]) >> (h & 31)) & 1u) != 0
-                                : a.labels[h] == kUnset;
+          const bool alive = BM ? is_alive(a, h) : a.labels[h] == kUnset;
           if (alive) {
             const uint32_t old = atomicSub(&a.deg[h], c);
             cross = old > b32r && old - c <= b32r;
+            lx = old >= s.kth && old - c < s.kth;
           }
         }
+        stage_low(lx, h, s, a, s.klb);
         const uint32_t cm = __ballot_sync(~0u, cross);
         if (cm) {
           uint32_t base = 0;
@@ -661,7 +879,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     }
     if (PROF && P && rounds <= 4096) {
       a.rtrace[3 * (rounds - 1)] = clock64() - tp;
-      a.rtrace[3 * (rounds - 1) + 1] = Fc;
+      a.rtrace[3 * (rounds - 1) + 1] = Fc | ((remaining + Fc) << 32);  // alive at round start
       a.rtrace[3 * (rounds - 1) + 2] = Ftot;
     }
     mark(3);
@@ -761,6 +979,14 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   const uint64_t nch = (2 * g.m) / CH + 2;
   DevBuf<uint32_t> cse0(nch), cse1(nch);
   DevBuf<Acc> acc(3);
+  DevBuf<uint32_t> low0, low1, hist(NB);
+  DevBuf<unsigned long long> lt(2);
+  if (!approx) {
+    low0.alloc(n);
+    low1.alloc(n);
+  }
+  lt.zero();
+  hist.zero();
   DevBuf<GridBarrier> bar(1);
   DevBuf<uint32_t> out(3);
   out.zero();
@@ -778,6 +1004,7 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
 
   const size_t smem = sizeof(Smem);
   const bool prof = getenv("DG_KCORE_PROFILE") && getenv("DG_KCORE_PROFILE")[0] == '1';
+  const bool nolow = getenv("DG_KCORE_LOWLIST") && getenv("DG_KCORE_LOWLIST")[0] == '0';
   void* kfn = bm ? (prof ? (void*)k_coreness<true, true> : (void*)k_coreness<true, false>)
                  : (prof ? (void*)k_coreness<false, true> : (void*)k_coreness<false, false>);
   DG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -798,11 +1025,15 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
               {Frontier{v0.get(), fa0.get(), fo0.get(), cse0.get()},
                Frontier{v1.get(), fa1.get(), fo1.get(), cse1.get()}},
               acc.get(),
+              {low0.get(), low1.get()},
+              lt.get(),
+              hist.get(),
               bar.get(),
               out.get(),
               prof ? kcore_prof_buffer() + 8 : nullptr,
               prof ? kcore_prof_buffer() : nullptr,
               approx ? 1 : 0,
+              nolow ? 1 : 0,
               c_num,
               c_den};
   void* params[] = {&args};

@@ -30,12 +30,17 @@ print("  " + " ".join(f"{k}={p[i] / ghz / 1e3:.3f}ms" for i, k in enumerate(name
 
 R = int(r.trace.init.peel_rounds)
 tr = p[8:8 + 3 * min(R, 4096)].reshape(-1, 3).astype(np.int64)
-cyc, fc, ftot = tr[:, 0], tr[:, 1], tr[:, 2]
+cyc, fc, ftot = tr[:, 0], tr[:, 1] & 0xffffffff, tr[:, 2]
+alive = tr[:, 1] >> 32
 order = np.argsort(-cyc)
 print(f"  per-round expand: mean {cyc.mean()/ghz:.2f}us median {np.median(cyc)/ghz:.2f}us; "
       f"top-20 rounds hold {100*cyc[order[:20]].sum()/cyc.sum():.1f}% of expand time")
 for i in order[:8]:
-    print(f"    round {i+1}: {cyc[i]/ghz:.1f}us Fc={fc[i]} arcs={ftot[i]}")
+    print(f"    round {i+1}: {cyc[i]/ghz:.1f}us Fc={fc[i]} arcs={ftot[i]} alive={alive[i]}")
+for A in (16384, 32768, 65536, 131072):
+    sel = alive <= A
+    print(f"  rounds with <= {A} alive: {sel.sum()} taking {cyc[sel].sum()/ghz/1e3:.2f}ms expand, "
+          f"{ftot[sel].sum()/1e6:.0f}M arcs")
 small = ftot < 4096
 print(f"  rounds with < 4096 arcs: {small.sum()} taking {cyc[small].sum()/ghz/1e3:.2f}ms "
       f"({cyc[small].mean()/ghz:.2f}us each); others {(~small).sum()} taking {cyc[~small].sum()/ghz/1e3:.2f}ms")
@@ -43,8 +48,15 @@ print(f"  rounds with < 4096 arcs: {small.sum()} taking {cyc[small].sum()/ghz/1e
 L = int(p[6])
 lt = p[8 + 3 * 4096: 8 + 3 * 4096 + 3 * min(L, 4096)].reshape(-1, 3).astype(np.int64)
 lc, ll, lsp = lt[:, 0], lt[:, 1], lt[:, 2]
+full = (lsp >> 40) & 1 == 1
+lsp = lsp & ((1 << 40) - 1)
 print(f"  level passes: {L}, sum {lc.sum()/ghz/1e3:.3f}ms, entries scanned {ll.sum()/1e6:.1f}M, "
       f"spilled {lsp.sum()/1e6:.2f}M")
+print(f"    full passes (live list): {full.sum()}, {lc[full].sum()/ghz/1e3:.3f}ms, "
+      f"{ll[full].sum()/1e6:.1f}M entries; low-list passes: {(~full).sum()}, "
+      f"{lc[~full].sum()/ghz/1e3:.3f}ms, {ll[~full].sum()/1e6:.1f}M entries")
+for i in np.nonzero(full)[0][:12]:
+    print(f"      full pass {i}: {lc[i]/ghz:.1f}us entries={ll[i]}")
 for lo, hi in ((0, 10), (10, 50), (50, 200), (200, 100000)):
     sel = slice(lo, min(hi, L))
     if lo < L:
