@@ -381,10 +381,10 @@ KeyRange key_range(const dg_graph& g, const uint64_t* d_loads) {
 }
 
 // Per-row CTA slices for the cluster kernel: seg[v*(CS+1) + r] = index
-// inside row v of its first neighbour >= r * nc (rows ascend), one thread
-// per (row, r) by binary search.
+// inside row v of its first neighbour >= r * no (rows ascend; CTA r owns ids
+// [r*no, (r+1)*no)), one thread per (row, r) by binary search.
 template <int CS>
-__global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t n, uint32_t nc,
+__global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t n, uint32_t no,
                             uint32_t* seg) {
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * (CS + 1);
        i += uint64_t(gridDim.x) * blockDim.x) {
@@ -395,7 +395,7 @@ __global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t 
     if (r == 0) {
       hi = 0;
     } else if (r < CS) {
-      const uint32_t x = r * nc;
+      const uint32_t x = r * no;
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (adj[o0 + mid] < x) lo = mid + 1; else hi = mid;
@@ -408,7 +408,7 @@ __global__ void k_seg_table(const uint64_t* offs, const uint32_t* adj, uint64_t 
 // Cluster variant: returns false when no cluster configuration fits.
 template <int CS, int PT>
 bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
-                       uint32_t nc, uint32_t* d_perm, uint64_t* d_raw,
+                       uint32_t nc, uint32_t no, uint32_t* d_perm, uint64_t* d_raw,
                        unsigned long long* d_batches) {
   const uint64_t n = g.n;
   const bool offs32 = 2 * g.m < 0xffffffffULL;
@@ -452,10 +452,10 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
   DG_CUDA(cudaMemsetAsync(d_raw, 0, n * sizeof(uint64_t), stream()));
   DevBuf<uint32_t> seg(n * (CS + 1));
   k_seg_table<CS><<<grid_for(n * (CS + 1), 256), 256, 0, stream()>>>(g.offs.get(), g.adj.get(), n,
-                                                                      nc, seg.get());
+                                                                      no, seg.get());
   DG_CHECK_LAUNCH();
   peelc::Args a{g.offs.get(), g.adj.get(), uint32_t(n), d_loads, base, one ? 1 : 0,
-                nc, nc / PT, offs_smem ? 1 : 0, d_perm, d_raw, seg.get(),
+                nc, nc / PT, no, offs_smem ? 1 : 0, d_perm, d_raw, seg.get(),
                 slice_smem ? 1 : 0, d_batches, peel_prof_buffer()};
   DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   count_launch();
@@ -466,10 +466,12 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
 template <int CS>
 bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, bool one,
                     uint32_t* d_perm, uint64_t* d_raw, unsigned long long* d_batches) {
-  // NC ids per CTA: the smallest multiple of the CTA size covering n / CS, so
-  // every CTA of the cluster holds vertices (power-of-two blocks left 7 of 16
-  // CTAs empty on RMAT-26's 17.9K core); DG_CLUSTER_POW2=1 restores them.
-  const uint64_t per_cta = (g.n + CS - 1) / CS;
+  // NO = ceil(n / CS) ids owned per CTA, in NC key slots (the smallest
+  // multiple of the CTA size covering NO), so every CTA of the cluster holds
+  // the same share of the vertices (NO rounded up to a multiple of the CTA
+  // size left 4 of 16 CTAs empty on RMAT-26's 17.9K core, and power-of-two
+  // blocks 7); DG_CLUSTER_POW2=1 restores power-of-two blocks.
+  uint64_t per_cta = (g.n + CS - 1) / CS;
   // 512-thread CTAs up to 12 keys per thread (RMAT-26's 84K core: 3.72 vs
   // 3.78 us/batch at 1024), 1024 beyond
   int pt = per_cta <= 6144 ? 512 : 1024;
@@ -480,12 +482,15 @@ bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, b
     while (nc * CS < g.n) nc *= 2;
     if (nc < uint64_t(pt)) nc = pt;
     c = nc / pt;
+    per_cta = nc;
   }
   if (c > 32) return false;  // <= 32 keys per thread (the S1 match mask)
   const uint32_t nc = uint32_t(c * pt);
+  if (getenv("DG_CLUSTER_NCOWN") && getenv("DG_CLUSTER_NCOWN")[0] == '1') per_cta = nc;
+  const uint32_t no = uint32_t(per_cta);
   if (pt == 512)
-    return launch_cluster_pt<CS, 512>(g, d_loads, base, one, nc, d_perm, d_raw, d_batches);
-  return launch_cluster_pt<CS, 1024>(g, d_loads, base, one, nc, d_perm, d_raw, d_batches);
+    return launch_cluster_pt<CS, 512>(g, d_loads, base, one, nc, no, d_perm, d_raw, d_batches);
+  return launch_cluster_pt<CS, 1024>(g, d_loads, base, one, nc, no, d_perm, d_raw, d_batches);
 }
 
 void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,

@@ -71,8 +71,9 @@ struct Args {
   const uint64_t* loads;
   uint64_t base;
   int one;
-  uint32_t nc;     // NC ids per CTA (a multiple of PT)
+  uint32_t nc;     // NC key slots per CTA (a multiple of PT)
   uint32_t chunk;  // keys per thread = NC / PT (<= 32)
+  uint32_t no;     // NO <= NC ids owned per CTA: [rank*NO, (rank+1)*NO)
   int offs_smem;   // row offsets staged in shared memory (u32)
   uint32_t* perm;
   uint64_t* raw;   // zeroed by the launcher
@@ -255,6 +256,26 @@ __device__ __forceinline__ void remove_flat(const uint4* adj4, uint32_t keys_s, 
   }
 }
 
+// S1 over KR >= c keys held in registers: retire this thread's batch marks,
+// then the minimum and the mask of keys at it
+template <int KR, class R>
+__device__ __forceinline__ void scan_regs(uint32_t* keys, uint32_t lo, uint32_t c, bool& marked,
+                                          uint32_t& lmin, uint32_t& bits) {
+  uint32_t k[KR];
+#pragma unroll
+  for (int j = 0; j < KR; ++j) k[j] = uint32_t(j) < c ? keys[lo + j] : R::DEAD;
+  if (marked) {
+#pragma unroll
+    for (int j = 0; j < KR; ++j)
+      if (uint32_t(j) < c && R::in_batch(k[j])) k[j] = keys[lo + j] = R::DEAD;
+    marked = false;
+  }
+#pragma unroll
+  for (int j = 0; j < KR; ++j) lmin = min(lmin, k[j]);
+#pragma unroll
+  for (int j = 0; j < KR; ++j) bits |= uint32_t(k[j] == lmin) << j;
+}
+
 template <int CS, int PT>
 __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   constexpr uint32_t NW = PT / 32;
@@ -265,6 +286,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   const uint32_t rank = cl.block_rank();
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t NC = a.nc;
+  const uint32_t NO = a.no;
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem);
   uint32_t* soffs = keys + NC;  // NC + 1 entries when staged
   const size_t head = (size_t(NC) * 4 * (a.offs_smem ? 2 : 1) + 4 + 15) & ~size_t(15);
@@ -274,22 +296,23 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   const uint4* adj4 = reinterpret_cast<const uint4*>(a.adj);
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
   const uint32_t n = a.n, c = a.chunk, lo = tid * c, hi = lo + c;
-  const uint32_t gbase = rank * NC;  // first global id owned by this CTA
+  const uint32_t gbase = rank * NO;  // first global id owned by this CTA
   const bool vec = (c & 3u) == 0;
   const uint32_t keys_s = smem_u32(keys);
 
+  const uint32_t gend = min(n, gbase + NO);  // end of the owned range
   for (uint32_t i = lo; i < hi; ++i) {
     const uint32_t g = gbase + i;
-    if (g < n) {
+    if (g < gend) {
       const uint64_t o0 = a.offs[g], o1 = a.offs[g + 1];
       keys[i] = uint32_t(a.loads[g] - a.base + (o1 - o0));
       if (a.offs_smem) soffs[i] = uint32_t(o0);
     } else {
       keys[i] = R::DEAD;
-      if (a.offs_smem) soffs[i] = uint32_t(a.offs[n]);
+      if (a.offs_smem) soffs[i] = uint32_t(a.offs[gend]);
     }
   }
-  if (a.offs_smem && tid == 0) soffs[NC] = uint32_t(a.offs[min(n, gbase + NC)]);
+  if (a.offs_smem && tid == 0) soffs[NC] = uint32_t(a.offs[gend]);
   if (PT == 512 && a.slice_smem)  // removal reads its row slices without a global round trip
     for (uint32_t v = tid; v < n; v += PT) {
       const uint32_t* sg = a.seg + size_t(v) * (CS + 1) + rank;
@@ -341,15 +364,23 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     const uint32_t par = uint32_t(nbat & 1);
     const uint32_t mbA = smem_u32(&s.mbA[par]), mbB = smem_u32(&s.mbB[par]);
     // ---- retire my BATCH marks (no decrement of this CTA's keys runs
-    // between the last CTA barrier and the next removal)
-    if (marked) {
-      for (uint32_t i = lo; i < hi; ++i)
-        if (R::in_batch(keys[i])) keys[i] = R::DEAD;
-      marked = false;
-    }
+    // between the last CTA barrier and the next removal), then
     // ---- S1: CTA summary
     uint32_t lmin = R::DEAD, bits = 0;  // bits: my keys at lmin (chunk <= 32)
-    if (vec) {
+    // up to 8 keys per thread: one round of loads into registers serves the
+    // retirement, the minimum and the match mask (17.9K core: 2.37 -> 1.99
+    // us/batch against reloading the keys for each; a register array of the
+    // exact tier, since predicated slots cost issue slots on every batch)
+    if (c <= 4) {
+      scan_regs<4, R>(keys, lo, c, marked, lmin, bits);
+    } else if (PT == 512 && c <= 8) {
+      scan_regs<8, R>(keys, lo, c, marked, lmin, bits);
+    } else if (vec) {
+      if (marked) {
+        for (uint32_t i = lo; i < hi; ++i)
+          if (R::in_batch(keys[i])) keys[i] = R::DEAD;
+        marked = false;
+      }
       const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
       for (uint32_t q = 0; q < (c >> 2); ++q) {
         const uint4 v = kv[q];
@@ -362,6 +393,11 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
                 << (4 * q);
       }
     } else {
+      if (marked) {
+        for (uint32_t i = lo; i < hi; ++i)
+          if (R::in_batch(keys[i])) keys[i] = R::DEAD;
+        marked = false;
+      }
       for (uint32_t i = lo; i < hi; ++i) lmin = min(lmin, keys[i]);
       for (uint32_t i = lo; i < hi; ++i) bits |= uint32_t(keys[i] == lmin) << (i - lo);
     }
@@ -377,8 +413,10 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       s.wcnt[w] = wc;
       s.wfirst[w] = wf;
     }
+    stamp(nbat, 5);
     if (tid == 0) mbar_expect(mbA, CS * uint32_t(sizeof(Summary)));
     __syncthreads();
+    stamp(nbat, 6);
     if (w == 0) {  // CTA summary, pushed to every CTA (lane q -> CTA q)
       const uint32_t x = lane < NW ? s.wmin[lane] : R::DEAD;
       const uint32_t cm = __reduce_min_sync(~0u, x);
@@ -409,6 +447,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
                      : "memory");
       }
 #endif
+      stamp(nbat, 7);
       if (lane < CS) {
         const uint32_t dst = mapa(smem_u32(&s.sum[par][rank]), lane);
         const uint32_t bar = mapa(mbA, lane);
@@ -476,13 +515,13 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         }
         unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
         if (bs == 1)
-          remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
+          remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
         else
-          remove_local<false, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NC, rawj);
+          remove_local<false, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
       } else if constexpr (NW < 32) {  // lane j <- member j (the owner lane of rank j)
         const uint32_t lj = (lane < bs ? __fns(ownmask, 0, int(lane) + 1) : 0u) & 31u;
         remove_flat<PT>(adj4, keys_s, bs, __shfl_sync(~0u, rfirst, lj), __shfl_sync(~0u, rdeg, lj),
-                    __shfl_sync(~0u, rr0, lj), w, lane, gbase, NC,
+                    __shfl_sync(~0u, rr0, lj), w, lane, gbase, NO,
                     reinterpret_cast<unsigned long long*>(&a.raw[pos]));
       }
       if (P) {
@@ -550,7 +589,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           slice_of(mj.v, s0, s1);
           remove_local<false, UQ>(adj4, keys_s,
                                   (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, s1 - s0,
-                                  mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NC,
+                                  mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NO,
                                   reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
         } else if constexpr (NW < SB) {
           Member mj = {0u, 0u, 0u, 0u};
@@ -560,7 +599,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
             slice_of(mj.v, s0, s1);
           }
           remove_flat<PT>(adj4, keys_s, bs, mj.v, s1 - s0,
-                          (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, w, lane, gbase, NC,
+                          (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, w, lane, gbase, NO,
                           reinterpret_cast<unsigned long long*>(&a.raw[pos]));
         }
         __syncthreads();
@@ -584,7 +623,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
               o = a.offs[mv];
               slice_of(mv, s0, s1);
             }
-            remove_flat<PT>(adj4, keys_s, gb, mv, s1 - s0, o + s0, w, lane, gbase, NC,
+            remove_flat<PT>(adj4, keys_s, gb, mv, s1 - s0, o + s0, w, lane, gbase, NO,
                             reinterpret_cast<unsigned long long*>(&a.raw[pos + g0]));
           }
         } else {
@@ -596,7 +635,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
             const uint64_t oj = a.offs[vj];
             uint32_t s0, s1;
             slice_of(vj, s0, s1);
-            remove_local<false, UQ>(adj4, keys_s, oj + s0, s1 - s0, vj, 0, 1, lane, gbase, NC,
+            remove_local<false, UQ>(adj4, keys_s, oj + s0, s1 - s0, vj, 0, 1, lane, gbase, NO,
                                     reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
           }
         }

@@ -25,8 +25,8 @@ t = buf[: 8 * 16 * 8].reshape(8, 16, 8).astype(np.int64)
 it = r.trace.iters[-1]
 print(f"scale {scale} T={T}: last iteration n={it.n} batches={it.batches} "
       f"{1e3 * it.order_ms / it.batches:.2f} us/batch; batches {first}..{first + 7}")
-phases = ["push", "wait", "remove", "tail", "total"]
-acc = np.zeros((16, 5))
+phases = ["push", "wait", "remove", "tail", "total", "scan", "bar", "w0red", "send"]
+acc = np.zeros((16, 9))
 nsimple = 0
 for b in range(8):
     row = []
@@ -35,7 +35,7 @@ for b in range(8):
     for q in range(16):
         s = t[b, q]
         d = [s[1] - s[0], s[2] - s[1], (s[3] - s[2]) if simple else 0, (s[4] - s[3]) if simple else 0,
-             s[4] - s[0]]
+             s[4] - s[0], s[5] - s[0], s[6] - s[5], s[7] - s[6], s[1] - s[7]]
         if simple:
             acc[q] += d
         row.append(d)
