@@ -344,9 +344,34 @@ __global__ void __launch_bounds__(LB, 1) k_peel(Args<K> a) {
       a.raw[pend_pos + t] = uint64_t(pend_key) - pend_cnt[t];
       if (pend_reset) pend_cnt[t] = 0;
     }
+    // compile-time chunks of <= 16 u32 keys (no COOP) stay in registers
+    // across the retirement and S1: one round of shared loads per batch
+    constexpr bool REGS = VQ > 0 && VQ <= 4 && sizeof(K) == 4;
+    uint4 kr[REGS ? VQ : 1];
+    if constexpr (REGS) {
+      const uint4* kv = reinterpret_cast<const uint4*>(keys) + (lo >> 2);
+#pragma unroll
+      for (int q = 0; q < VQ; ++q) kr[q] = kv[q];
+    }
     // ---- retire my BATCH marks of the previous batch (no decrements run
     // between barrier C and barrier A, so the read-modify-write is safe)
-    if (marked) {
+    if (REGS && marked) {
+      uint4* kv = reinterpret_cast<uint4*>(keys) + (lo >> 2);
+#pragma unroll
+      for (int q = 0; q < (REGS ? VQ : 0); ++q) {
+        uint4& v = kr[q];
+        const bool hit = R::in_batch(K(v.x)) | R::in_batch(K(v.y)) | R::in_batch(K(v.z)) |
+                         R::in_batch(K(v.w));
+        if (hit) {
+          if (R::in_batch(K(v.x))) v.x = uint32_t(R::DEAD);
+          if (R::in_batch(K(v.y))) v.y = uint32_t(R::DEAD);
+          if (R::in_batch(K(v.z))) v.z = uint32_t(R::DEAD);
+          if (R::in_batch(K(v.w))) v.w = uint32_t(R::DEAD);
+          kv[q] = v;
+        }
+      }
+      marked = false;
+    } else if (marked) {
       if constexpr (VQ > 0 && sizeof(K) == 4) {
         uint4* kv = reinterpret_cast<uint4*>(keys) + (lo >> 2);
 #pragma unroll
@@ -396,7 +421,25 @@ __global__ void __launch_bounds__(LB, 1) k_peel(Args<K> a) {
       if (!R::alive(lmin)) lmin = R::DEAD;
       lcnt = R::alive(lmin) ? 1u : 0u;
     } else {
-      if (lo < n) chunk_min_count<VQ>(keys, lo, c, lmin, lcnt, lfirst);  // padding: skip
+      if constexpr (REGS) {
+        if (lo < n) {  // padding: skip
+          uint32_t m = 0xffffffffu;
+#pragma unroll
+          for (int q = 0; q < (REGS ? VQ : 0); ++q)
+            m = min(min(m, min(kr[q].x, kr[q].y)), min(kr[q].z, kr[q].w));
+          uint32_t mask = 0;
+#pragma unroll
+          for (int q = 0; q < (REGS ? VQ : 0); ++q)
+            mask |= ((kr[q].x == m) | ((kr[q].y == m) << 1) | ((kr[q].z == m) << 2) |
+                     (uint32_t(kr[q].w == m) << 3))
+                    << (4 * q);
+          lmin = K(m);
+          lcnt = uint32_t(__popc(mask));
+          lfirst = lo + uint32_t(__ffs(mask)) - 1;
+        }
+      } else if (lo < n) {
+        chunk_min_count<VQ>(keys, lo, c, lmin, lcnt, lfirst);  // padding: skip
+      }
       if (!R::alive(lmin)) {  // nothing alive in my chunk
         lmin = R::DEAD;
         lcnt = 0;
