@@ -102,9 +102,10 @@ struct Fixed {
   unsigned long long mbA[2], mbB[2];  // summaries / staged members, by parity
   Summary sum[2][16];                 // [parity][CTA rank]
   Member stage[2][SB];                // [parity][member]
-  uint32_t wmin[MAXW];
-  uint32_t wcnt[MAXW];
-  uint32_t wfirst[MAXW];
+  // per-warp summary: {min key, #keys at it, first index at it, its row start}
+  // and that row's degree (row bounds only with offsets staged in shared memory)
+  uint4 wsum[MAXW];
+  uint32_t wdeg[MAXW];
   // warp -> member map over this CTA's warps for batches of b <= SB members:
   // wmap[b-1][w] = j | rank << 8 | nwj << 16 (j = w % b, rank = w / b,
   // nwj = #warps serving member j); batches of more than NW members are
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   const unsigned long long arm = (DG_PEEL_PROF && a.prof) ? a.prof[15] : 0ULL;
   auto stamp = [&](unsigned long long b, int k) {
     if (DG_PEEL_PROF && tid == 0 && arm && b + 1 >= arm && b + 1 < arm + 8)
-      a.prof[16 + ((b + 1 - arm) * 16 + rank) * 8 + k] = clock64();
+      a.prof[16 + ((b + 1 - arm) * 16 + rank) * 12 + k] = clock64();
   };
   long long c1 = 0, c2 = 0, c3 = 0, tm = DG_PEEL_PROF ? clock64() : 0;
   while (removed < n) {
@@ -404,34 +405,38 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     uint32_t lcnt = __popc(bits);
     const uint32_t lfirst = lo + __ffs(bits) - 1;
     if (!R::alive(lmin)) lmin = R::DEAD, lcnt = 0;
+    // my first minimum's row bounds, loaded while the warp reduces (the CTA
+    // summary then needs no dependent shared loads after the barrier)
+    uint32_t q0 = 0, q1 = 0;
+    if (a.offs_smem) {
+      q0 = soffs[lfirst];
+      q1 = soffs[lfirst + 1];
+    }
     const uint32_t wm = __reduce_min_sync(~0u, lmin);
-    const uint32_t wc = __reduce_add_sync(~0u, lmin == wm ? lcnt : 0u);
     const uint32_t fl = __ffs(__ballot_sync(~0u, lmin == wm)) - 1;
-    const uint32_t wf = __shfl_sync(~0u, lfirst, fl);
-    if (lane == 0) {
-      s.wmin[w] = wm;
-      s.wcnt[w] = wc;
-      s.wfirst[w] = wf;
+    const uint32_t wc = __reduce_add_sync(~0u, lmin == wm ? lcnt : 0u);
+    if (lane == fl) {
+      s.wsum[w] = make_uint4(wm, wc, lfirst, q0);
+      s.wdeg[w] = q1 - q0;
     }
     stamp(nbat, 5);
     if (tid == 0) mbar_expect(mbA, CS * uint32_t(sizeof(Summary)));
     __syncthreads();
     stamp(nbat, 6);
     if (w == 0) {  // CTA summary, pushed to every CTA (lane q -> CTA q)
-      const uint32_t x = lane < NW ? s.wmin[lane] : R::DEAD;
+      const uint4 ws = lane < NW ? s.wsum[lane] : make_uint4(R::DEAD, 0u, 0u, 0u);
+      const uint32_t wd = lane < NW ? s.wdeg[lane] : 0u;
+      const uint32_t x = ws.x;
       const uint32_t cm = __reduce_min_sync(~0u, x);
-      const uint32_t ccnt = __reduce_add_sync(~0u, x == cm ? s.wcnt[lane] : 0u);
       const uint32_t fw = __ffs(__ballot_sync(~0u, x == cm)) - 1;
-      const uint32_t f = s.wfirst[fw];
-      uint64_t r0 = 0, r1 = 0;
-      if (R::alive(cm)) {
-        if (a.offs_smem) {
-          r0 = soffs[f];
-          r1 = soffs[f + 1];
-        } else {
-          r0 = a.offs[gbase + f];
-          r1 = a.offs[gbase + f + 1];
-        }
+      const uint32_t ccnt = __reduce_add_sync(~0u, x == cm ? ws.y : 0u);
+      const uint32_t f = __shfl_sync(~0u, ws.z, fw);
+      uint64_t r0 = __shfl_sync(~0u, ws.w, fw), r1 = r0 + __shfl_sync(~0u, wd, fw);
+      if (!R::alive(cm)) {
+        r0 = r1 = 0;
+      } else if (!a.offs_smem) {
+        r0 = a.offs[gbase + f];
+        r1 = a.offs[gbase + f + 1];
       }
 #if DG_ROW_PREFETCH
       // the CTA's candidate is a likely member of this or an early batch:
@@ -514,6 +519,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           dj = s1 - s0;
         }
         unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
+        stamp(nbat, 8);
         if (bs == 1)
           remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
         else
@@ -536,8 +542,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       if (tid == 0 && bs <= SB) mbar_expect(mbB, bs * uint32_t(sizeof(Member)));
       if (((ownmask >> rank) & 1u) && wm == gmin) {  // this warp owns part of the batch
         const uint32_t cta_off = __reduce_add_sync(~0u, (lane < rank && own) ? rcnt : 0u);
-        const uint32_t xw = lane < NW ? s.wmin[lane] : R::DEAD;
-        const uint32_t woff = __reduce_add_sync(~0u, (lane < w && xw == gmin) ? s.wcnt[lane] : 0u);
+        const uint4 wsl = lane < NW ? s.wsum[lane] : make_uint4(R::DEAD, 0u, 0u, 0u);
+        const uint32_t woff = __reduce_add_sync(~0u, (lane < w && wsl.x == gmin) ? wsl.y : 0u);
         const bool mine = lmin == gmin && lcnt;
         const uint32_t mm = __ballot_sync(~0u, mine);
         uint32_t my = cta_off + woff;

@@ -21,12 +21,12 @@ r = dg.run(g, dg.RunConfig(iterations=T))
 dg.diag().dg_peel_trace_arm(0xFFFFFFFF)
 buf = np.zeros(8 * 32 * 12, np.uint64)
 dg.diag().dg_peel_trace_read(buf.ctypes.data_as(C.POINTER(C.c_uint64)))
-t = buf[: 8 * 16 * 8].reshape(8, 16, 8).astype(np.int64)
+t = buf[: 8 * 16 * 12].reshape(8, 16, 12).astype(np.int64)
 it = r.trace.iters[-1]
 print(f"scale {scale} T={T}: last iteration n={it.n} batches={it.batches} "
       f"{1e3 * it.order_ms / it.batches:.2f} us/batch; batches {first}..{first + 7}")
-phases = ["push", "wait", "remove", "tail", "total", "scan", "bar", "w0red", "send"]
-acc = np.zeros((16, 9))
+phases = ["push", "wait", "remove", "tail", "total", "scan", "bar", "w0red", "send", "decode", "rm_rows"]
+acc = np.zeros((16, 11))
 nsimple = 0
 for b in range(8):
     row = []
@@ -35,7 +35,8 @@ for b in range(8):
     for q in range(16):
         s = t[b, q]
         d = [s[1] - s[0], s[2] - s[1], (s[3] - s[2]) if simple else 0, (s[4] - s[3]) if simple else 0,
-             s[4] - s[0], s[5] - s[0], s[6] - s[5], s[7] - s[6], s[1] - s[7]]
+             s[4] - s[0], s[5] - s[0], s[6] - s[5], s[7] - s[6], s[1] - s[7],
+             (s[8] - s[2]) if simple else 0, (s[3] - s[8]) if simple else 0]
         if simple:
             acc[q] += d
         row.append(d)
