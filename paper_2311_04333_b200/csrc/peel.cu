@@ -472,9 +472,10 @@ bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, b
   // size left 4 of 16 CTAs empty on RMAT-26's 17.9K core, and power-of-two
   // blocks 7); DG_CLUSTER_POW2=1 restores power-of-two blocks.
   uint64_t per_cta = (g.n + CS - 1) / CS;
-  // 512-thread CTAs up to 12 keys per thread (RMAT-26's 84K core: 3.72 vs
-  // 3.78 us/batch at 1024), 1024 beyond
-  int pt = per_cta <= 6144 ? 512 : 1024;
+  // 512-thread CTAs while their keys fit S1's 8-key register tier, 1024
+  // beyond (RMAT-26's 84K core, 5.2K ids per CTA: 3.50 us/batch at 1024 with
+  // 6 keys per thread in registers vs 3.55 at 512 with 11 keys reloaded)
+  int pt = per_cta <= 4096 ? 512 : 1024;
   if (const char* e = getenv("DG_CLUSTER_PT")) pt = atoi(e) == 512 ? 512 : 1024;
   uint64_t c = (per_cta + pt - 1) / pt;  // keys per thread
   if (getenv("DG_CLUSTER_POW2") && getenv("DG_CLUSTER_POW2")[0] == '1') {

@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     // exact tier, since predicated slots cost issue slots on every batch)
     if (c <= 4) {
       scan_regs<4, R>(keys, lo, c, marked, lmin, bits);
-    } else if (PT == 512 && c <= 8) {
+    } else if (c <= 8) {
       scan_regs<8, R>(keys, lo, c, marked, lmin, bits);
     } else if (vec) {
       if (marked) {
