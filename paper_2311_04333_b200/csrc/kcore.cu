@@ -44,7 +44,7 @@ constexpr uint32_t CH = 32;     // arcs per chunk = one warp step
 constexpr int UC = 2;           // chunks in flight per warp (short-row steps)
 constexpr int SC = 8;           // chunks per super-chunk (one warp step on long rows)
 #ifndef DG_KC_HUBS
-#define DG_KC_HUBS 8192         // big rounds: decrements of ids below this summed per CTA
+#define DG_KC_HUBS 4096         // big rounds: decrements of ids below this summed per CTA
 #endif
 constexpr uint32_t HUBS = DG_KC_HUBS;
 #ifndef DG_KC_BUF
