@@ -100,6 +100,7 @@ struct KcArgs {
   unsigned long long* prof;    // [8] block-0 cycles (see dg_kcore_profile)
   int approx;
   int nolow;  // DG_KCORE_LOWLIST=0: no low list (every level advance a full pass)
+  uint64_t lowmin;  // live-list length from which level advances use the low list
   uint64_t c_num, c_den;
 };
 
@@ -542,7 +543,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       const uint64_t win = bound + LW;
       const bool track = !a.approx;
       // a low list pays while a full pass takes several tiles per CTA
-      const bool lowok = track && !a.nolow && livec >= 2ULL * gridDim.x * blockDim.x * LE;
+      const bool lowok = track && !a.nolow && livec >= a.lowmin;
       uint64_t Lc = 0;
       if (lowok) {
         if (threadIdx.x == 0) s.b_lc = ld_relaxed_u64(&a.lt[lb]);
@@ -1005,6 +1006,10 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
   const size_t smem = sizeof(Smem);
   const bool prof = getenv("DG_KCORE_PROFILE") && getenv("DG_KCORE_PROFILE")[0] == '1';
   const bool nolow = getenv("DG_KCORE_LOWLIST") && getenv("DG_KCORE_LOWLIST")[0] == '0';
+  // the low list pays once a full level pass takes two tiles per CTA;
+  // DG_KCORE_LOWMIN=<entries> overrides (tests drive it on small graphs)
+  uint64_t lowmin = 2ULL * num_sms() * KC_THREADS * LE;
+  if (const char* e = getenv("DG_KCORE_LOWMIN")) lowmin = strtoull(e, nullptr, 10);
   void* kfn = bm ? (prof ? (void*)k_coreness<true, true> : (void*)k_coreness<true, false>)
                  : (prof ? (void*)k_coreness<false, true> : (void*)k_coreness<false, false>);
   DG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1034,6 +1039,7 @@ CoreOut coreness(const dg_graph& g, bool approx, uint64_t c_num, uint64_t c_den,
               prof ? kcore_prof_buffer() : nullptr,
               approx ? 1 : 0,
               nolow ? 1 : 0,
+              lowmin,
               c_num,
               c_den};
   void* params[] = {&args};

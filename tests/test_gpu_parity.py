@@ -526,6 +526,36 @@ print("ok")
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("bitmap", ["1", "0"])
+def test_coreness_low_list_paths(orc, bitmap):
+    """Level advances through the low list (kcore.cu: theta from a sampled
+    degree histogram, theta crossings staged per CTA, dry lists falling back
+    to a full pass) forced on small graphs with DG_KCORE_LOWMIN, with and
+    without the alive bitmap: labels, kmax, peel_rounds equal the reference
+    restatement's (core.cpp:89-119) on three graph families."""
+    code = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "oracle"))
+import paper_2311_04333_b200 as dg
+from oracle import Oracle
+orc = Oracle()
+for u, v in (orc.gen_rmat(18, 16 << 18, 7), orc.gen_chung_lu(300000, 2000000, 5),
+             orc.gen_er_planted(80000, 600000, 300, 2)):
+    h = orc.build(u, v)
+    g = dg.Graph.from_pairs(u, v)
+    d = dg.exact_coreness(g)
+    lab, kmax, rounds = orc.coreness(h)
+    assert np.array_equal(d.labels, lab) and (d.kmax, d.peel_rounds) == (kmax, rounds)
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DG_KCORE_BITMAP=bitmap, DG_KCORE_LOWMIN="1", ROOT=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
 def _parse_device(dg, raw: bytes, off: int):
     """dg_parse_edge_list on device text starting `off` bytes into an allocation."""
     import ctypes as C
