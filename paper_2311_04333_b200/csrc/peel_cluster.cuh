@@ -263,8 +263,16 @@ template <int KR, class R>
 __device__ __forceinline__ void scan_regs(uint32_t* keys, uint32_t lo, uint32_t c, bool& marked,
                                           uint32_t& lmin, uint32_t& bits) {
   uint32_t k[KR];
+  if (KR == 8 && c == 8) {  // two 16-byte vectors (lo is a multiple of 4)
 #pragma unroll
-  for (int j = 0; j < KR; ++j) k[j] = uint32_t(j) < c ? keys[lo + j] : R::DEAD;
+    for (int q = 0; q < KR / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4*>(keys + lo)[q];
+      k[4 * q] = v.x, k[4 * q + 1] = v.y, k[4 * q + 2] = v.z, k[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < KR; ++j) k[j] = uint32_t(j) < c ? keys[lo + j] : R::DEAD;
+  }
   if (marked) {
 #pragma unroll
     for (int j = 0; j < KR; ++j)
