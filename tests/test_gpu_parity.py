@@ -527,6 +527,34 @@ print("ok")
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [30000, 45000, 60000, 75000, 120000])
+def test_peel_cluster_chunk_tiers(dg, orc, n):
+    """The cluster Greedy++ kernel (mode 2) across its S1 register tiers and
+    CTA sizes: per-CTA blocks of ceil(n/16) ids give 4, 6 and 8 keys per
+    thread at 512 threads (8: the two-vector load) and 5 and 8 at 1024
+    threads; the peel order (batch and one-at-a-time) and loads over three
+    Greedy++ iterations equal the reference restatement's (refine.cpp:20-220)."""
+    u, v = orc.gen_er_planted(n, 10 * n, 60, n % 97)
+    h = orc.build(u, v)
+    g = dg.Graph.from_csr(h.offs, h.adj, h.orig)
+    rng = np.random.default_rng(n)
+    ld = rng.integers(0, 48, h.n).astype(np.uint64)
+    lh = ld.copy()
+    dg.set_peel_mode(2)
+    try:
+        for it in range(3):
+            p = dg.load_peel_order(g, ld).perm
+            assert np.array_equal(p, orc.peel_order(h, lh, False)), (n, it)
+            dg.density_and_load_update(g, p, ld)
+            _, lh, _, _ = orc.density_update(h, p, lh)
+            assert np.array_equal(ld, lh), (n, it)
+        p = dg.load_peel_order(g, ld, one_at_a_time=True).perm
+        assert np.array_equal(p, orc.peel_order(h, lh, True)), n
+    finally:
+        dg.set_peel_mode(0)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("bitmap", ["1", "0"])
 def test_coreness_low_list_paths(orc, bitmap):
     """Level advances through the low list (kcore.cu: theta from a sampled

@@ -41,6 +41,9 @@ for A in (16384, 32768, 65536, 131072):
     sel = alive <= A
     print(f"  rounds with <= {A} alive: {sel.sum()} taking {cyc[sel].sum()/ghz/1e3:.2f}ms expand, "
           f"{ftot[sel].sum()/1e6:.0f}M arcs")
+for lim in (1024, 4096, 16384, 65536, 262144):
+    sel = ftot < lim
+    print(f"  rounds with < {lim} arcs: {sel.sum()} ({cyc[sel].sum()/ghz/1e3:.2f} ms expand)")
 small = ftot < 4096
 print(f"  rounds with < 4096 arcs: {small.sum()} taking {cyc[small].sum()/ghz/1e3:.2f}ms "
       f"({cyc[small].mean()/ghz:.2f}us each); others {(~small).sum()} taking {cyc[~small].sum()/ghz/1e3:.2f}ms")
