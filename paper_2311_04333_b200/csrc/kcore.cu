@@ -37,6 +37,9 @@ namespace dgb {
 namespace {
 
 constexpr int KC_THREADS = 1024;
+#ifndef DG_KC_SPEC
+#define DG_KC_SPEC 1
+#endif
 #ifndef DG_KC_COLD
 #define DG_KC_COLD __forceinline__
 #endif
@@ -239,7 +242,7 @@ __device__ DG_KC_COLD void level_pass(const KcArgs& a, Smem& s, const uint32_t* 
                                            uint32_t* live_out, uint64_t livec, bool implicit,
                                            uint64_t win, bool track, Acc* acc,
                                            unsigned long long* out_ctr, bool hist, uint32_t hb,
-                                           uint32_t& lmin) {
+                                           uint32_t& lmin, const Frontier* spec = nullptr) {
   const uint32_t lane = lane_id();
   const uint64_t tile = uint64_t(blockDim.x) * E;
   const uint64_t stride = LOCAL ? tile : uint64_t(gridDim.x) * tile;
@@ -263,8 +266,6 @@ __device__ DG_KC_COLD void level_pass(const KcArgs& a, Smem& s, const uint32_t* 
       d[e] = kUnset;
       if (i0 + e < livec) {
         const uint32_t x = v[e];
-        // the degree is read alongside the liveness word (not after it): one
-        // dependent round trip per entry instead of two
         // the degree is read alongside the liveness word (not after it): one
         // dependent round trip per entry instead of two
         const uint32_t dx = a.deg[x];
@@ -323,6 +324,21 @@ __device__ DG_KC_COLD void level_pass(const KcArgs& a, Smem& s, const uint32_t* 
     for (int e = 0; e < E; ++e)
       if (alive[e]) live_out[o++] = v[e];
     __syncthreads();  // s.baseL / ws32 reuse
+    if (E == 1 && spec) {
+      // speculative frontier (exact mode, short lists): the next bound is at
+      // least hb, so if any alive vertex has degree hb the new frontier is
+      // exactly the alive vertices of degree hb -- emitted here, before the
+      // pass's grid barrier, so that advance needs no second barrier; with
+      // none anywhere nothing is emitted and the usual emission follows
+      const bool isF = alive[0] && d[0] == hb;
+      uint64_t ro = 0;
+      uint32_t dl = 0;
+      if (isF) {
+        ro = a.offs[v[0]];
+        dl = uint32_t(a.offs[v[0] + 1] - ro);
+      }
+      emit_front_tile(isF, v[0], dl, ro, hb, a, *spec, acc, s);
+    }
   }
 }
 
@@ -552,6 +568,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
       }
       bool full = !lowok || Lc == 0;
       const uint32_t hb = uint32_t(bound) + 1;  // every alive degree is > bound here
+      bool spec = false;  // the last pass emitted the frontier of bound hb speculatively
       for (;;) {
         if (threadIdx.x == 0) {
           s.cnt = 0;
@@ -577,17 +594,21 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           octr = &a.lt[lb ^ 1];
         }
         const bool hist = full && lowok;
+        // short lists (one tile per CTA, exact mode): emit the frontier of
+        // bound hb speculatively during the pass (see level_pass)
+        spec = DG_KC_SPEC && track && !hist && cnt <= uint64_t(gridDim.x) * blockDim.x;
+        const Frontier* fsp = spec ? &a.fr[f & 1] : nullptr;
         // wide tiles only while the list fills the grid LE times over
         if (cnt >= uint64_t(gridDim.x) * blockDim.x * LE)
           level_pass<BM, LE>(a, s, in, out, cnt, imp, win, track, acc, octr, hist, hb, lmin);
         else
-          level_pass<BM, 1>(a, s, in, out, cnt, imp, win, track, acc, octr, hist, hb, lmin);
+          level_pass<BM, 1>(a, s, in, out, cnt, imp, win, track, acc, octr, hist, hb, lmin, fsp);
         // the low-list entries this CTA staged since the last level advance
         // (kept in shared memory, no per-round flush) join the pass; a full
         // pass rebuilds the list, so it drops them
         if (!full) {
           level_pass<BM, 1, true>(a, s, s.lid, out, min(s.lcnt, LB), false, win, track, acc, octr,
-                                  false, hb, lmin);
+                                  false, hb, lmin, fsp);
           if (threadIdx.x == 0) s.lcnt = 0;  // level_pass ended with a CTA barrier
         } else if (hist && threadIdx.x == 0) {
           s.lcnt = 0;
@@ -649,6 +670,8 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           t = nt;
         }
       }
+      // the speculative frontier is the frontier: no emission, no second barrier
+      const bool fast = spec && gmin == hb;
       const bool rebuild = full && lowok;
       if (full && !lowok && threadIdx.x == 0) s.kth = 0;  // no low list from here on
       if (rebuild) {
@@ -676,7 +699,9 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
         hist_dirty = true;
       }
       const Frontier& F0 = a.fr[f & 1];
-      if (track || bound <= win) {
+      if (fast) {
+        // s.b_front (fetched at the pass's barrier) holds the frontier
+      } else if (track || bound <= win) {
         // the frontier = candidates with residual degree <= bound: this CTA's
         // staged ones, then a grid-strided share of the spilled ones
         const uint32_t cnt = min(s.cnt, BUF);
