@@ -70,6 +70,7 @@ struct A3Args {
   uint64_t slack_samples, slack_allowed, slack_seed;
   uint64_t* suffix;
   Alg3Out* out;
+  uint64_t* cs;  // scratch: the charges A[i], n entries
 };
 
 __device__ __forceinline__ bool better(uint64_t e1, uint64_t v1, uint64_t i1, uint64_t e2,
@@ -106,22 +107,40 @@ __global__ void __launch_bounds__(PT, 1) k_alg3(A3Args a) {
   uint64_t badsum;
   block_excl_scan(bad, ws, &badsum);
 
-  // chunked suffix sums
+  // the charges, once, position-strided (coalesced perm / raw reads, four
+  // independent perm -> loads gathers in flight per thread) into scratch
+  uint64_t wmax = 0;
+  {
+    uint32_t i = tid;
+    for (; i + 3 * blockDim.x < n; i += 4 * blockDim.x) {
+      uint64_t x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[k] = charge(a, i + k * blockDim.x);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a.cs[i + k * blockDim.x] = x[k];
+        wmax = max(wmax, x[k]);
+      }
+    }
+    for (; i < n; i += blockDim.x) {
+      const uint64_t x = charge(a, i);
+      a.cs[i] = x;
+      wmax = max(wmax, x);
+    }
+  }
+  __syncthreads();  // scratch written by the whole block
+
+  // chunked suffix sums over the scratch copy
   const uint32_t c = (n + blockDim.x - 1) / blockDim.x;
   const uint32_t lo = min(n, tid * c), hi = min(n, lo + c);
   uint64_t local = 0;
-  uint64_t wmax = 0;
-  for (uint32_t i = lo; i < hi; ++i) {
-    const uint64_t x = charge(a, i);
-    local += x;
-    wmax = max(wmax, x);
-  }
+  for (uint32_t i = lo; i < hi; ++i) local += a.cs[i];
   uint64_t total;
   const uint64_t ex = block_excl_scan(local, ws, &total);
   uint64_t run = total - ex - local;  // sum of A beyond my chunk
   uint64_t be = 0, bv = 1, bi = ~0ULL;
   for (uint32_t i = hi; i-- > lo;) {
-    run += charge(a, i);
+    run += a.cs[i];
     if (a.suffix) a.suffix[i] = run;
     const uint64_t d = n - i;
     if (!dens_gt(be, bv, run, d)) {  // >= : walking down, smaller i wins ties
@@ -169,11 +188,9 @@ __global__ void __launch_bounds__(PT, 1) k_alg3(A3Args a) {
       a.out->slack_bad = badsum;
     }
   }
-  // loads += A (refine.cpp:213)
-  for (uint32_t i = lo; i < hi; ++i) {  // each thread owns its positions' loads
-    const uint64_t x = charge(a, i);
-    a.loads[a.perm[i]] += x;
-  }
+  // loads += A (refine.cpp:213); every position's vertex is distinct, and
+  // every charge was read before this point (the barrier above the scan)
+  for (uint32_t i = tid; i < n; i += blockDim.x) a.loads[a.perm[i]] += a.cs[i];
   __syncthreads();
   // next key range over vertices
   uint64_t mn = ~0ULL;
@@ -656,9 +673,10 @@ void alg3(const dg_graph& g, const uint32_t* d_perm, const uint32_t* d_charges,
           const uint64_t* d_raw, uint64_t raw_base, uint64_t* d_loads,
           uint64_t slack_samples, uint64_t slack_allowed, uint64_t slack_seed, uint64_t* d_suffix,
           Alg3Out* d_out) {
+  DevBuf<uint64_t> cs(g.n ? g.n : 1);
   A3Args a{g.offs.get(), uint32_t(g.n), d_perm, d_charges, d_raw, raw_base, d_loads,
            slack_samples, slack_allowed,
-           slack_seed, d_suffix, d_out};
+           slack_seed, d_suffix, d_out, cs.get()};
   k_alg3<<<1, PT, 0, stream()>>>(a);
   DG_CHECK_LAUNCH();
 }
