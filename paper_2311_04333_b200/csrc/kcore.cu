@@ -40,9 +40,6 @@ constexpr int KC_THREADS = 1024;
 #ifndef DG_KC_SPEC
 #define DG_KC_SPEC 1
 #endif
-#ifndef DG_KC_COLD
-#define DG_KC_COLD __forceinline__
-#endif
 constexpr uint32_t CH = 32;     // arcs per chunk = one warp step
 constexpr int UC = 2;           // chunks in flight per warp (short-row steps)
 constexpr int SC = 8;           // chunks per super-chunk (one warp step on long rows)
@@ -199,7 +196,7 @@ __device__ __forceinline__ void emit_front_tile(bool isF, uint32_t v, uint32_t d
 // Scan the live list: alive vertices with deg <= bound join the frontier,
 // the other alive ones are compacted into live_out.
 template <bool BM>
-__device__ DG_KC_COLD void collect(const KcArgs& a, uint32_t livec, bool implicit, const uint32_t* live_in,
+__device__ void collect(const KcArgs& a, uint32_t livec, bool implicit, const uint32_t* live_in,
                         uint32_t* live_out, uint32_t bound, uint32_t label, const Frontier& F,
                         Acc* acc, Smem& s, unsigned long long* live_ctr) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
@@ -238,7 +235,7 @@ __device__ DG_KC_COLD void collect(const KcArgs& a, uint32_t livec, bool implici
 // CTA's histogram s.hst[min(d - hb, NB - 1)] (full passes of exact mode).
 // LOCAL: the list is this CTA's own (shared memory), not a grid-strided share.
 template <bool BM, int E, bool LOCAL = false>
-__device__ DG_KC_COLD void level_pass(const KcArgs& a, Smem& s, const uint32_t* live_in,
+__device__ __forceinline__ void level_pass(const KcArgs& a, Smem& s, const uint32_t* live_in,
                                            uint32_t* live_out, uint64_t livec, bool implicit,
                                            uint64_t win, bool track, Acc* acc,
                                            unsigned long long* out_ctr, bool hist, uint32_t hb,
@@ -356,12 +353,7 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t x, uint32_t src) {
 // in the low list (staged in s.lid, flushed once per CTA at the end of the
 // round; theta = 0 outside exact mode: no alive degree is ever 0 before a
 // decrement).
-#ifdef DG_KC_NOINLINE_LOW
-__device__ __noinline__ void stage_low(
-#else
-__device__ __forceinline__ void stage_low(
-#endif
-bool lx, uint32_t uv, Smem& s, const KcArgs& a,
+__device__ __forceinline__ void stage_low(bool lx, uint32_t uv, Smem& s, const KcArgs& a,
                                           const uint32_t& lbs) {
   const uint32_t lm = __ballot_sync(~0u, lx);
   if (!lm) return;
@@ -407,11 +399,7 @@ __device__ __forceinline__ void expand_targets(const KcArgs& a, const uint32_t (
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const bool cross = live[k] && old[k] == b32 + 1;  // crossed: joins the next round
-#ifdef DG_KC_NOSTAGE
-    const bool lx = false;
-#else
     const bool lx = live[k] && old[k] == theta;       // crossed theta: joins the low list
-#endif
     if (!__any_sync(~0u, cross || lx)) continue;       // the usual case: one vote
     stage_low(lx, u[k], s, a, s.klb);
     const uint32_t cm = __ballot_sync(~0u, cross);
