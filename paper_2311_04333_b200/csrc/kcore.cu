@@ -149,6 +149,23 @@ __device__ __forceinline__ void fetch_acc(Smem& s, Acc* acc) {
 __device__ __forceinline__ bool is_alive(const KcArgs& a, uint32_t v) {
   return ((ld_relaxed_u32(&a.alive[v >> 5]) >> (v & 31)) & 1u) != 0;
 }
+#ifndef DG_ALIVE_LD
+#define DG_ALIVE_LD 1
+#endif
+// alive bit on the expansion path: may be stale (bits only ever clear, and a
+// decrement of a removed vertex never reports a crossing: its degree is
+// already at or below the bound), so it may come from L1
+__device__ __forceinline__ bool is_alive_exp(const KcArgs& a, uint32_t v) {
+  uint32_t w;
+#if DG_ALIVE_LD == 1
+  asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(w) : "l"(&a.alive[v >> 5]));
+#elif DG_ALIVE_LD == 2
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(w) : "l"(&a.alive[v >> 5]));
+#else
+  w = ld_relaxed_u32(&a.alive[v >> 5]);
+#endif
+  return ((w >> (v & 31)) & 1u) != 0;
+}
 
 // All threads of the CTA call this with a per-thread candidate (isF, v, d, o).
 // Publishes the tile's entries into the frontier with one atomic, labels
@@ -389,7 +406,7 @@ __device__ __forceinline__ void expand_targets(const KcArgs& a, const uint32_t (
       continue;
     }
     if (BM)
-      live[k] = is_alive(a, uv);  // removed?
+      live[k] = is_alive_exp(a, uv);  // removed?
     else
       live[k] = a.deg[uv] > b32;  // dead, or already at/below the bound
   }

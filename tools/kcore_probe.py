@@ -44,6 +44,13 @@ for A in (16384, 32768, 65536, 131072):
 for lim in (1024, 4096, 16384, 65536, 262144):
     sel = ftot < lim
     print(f"  rounds with < {lim} arcs: {sel.sum()} ({cyc[sel].sum()/ghz/1e3:.2f} ms expand)")
+print("  by round size (arcs): rounds, expand ms, us/round, G arcs/s")
+for lo in (0, 1 << 12, 1 << 14, 1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24, 1 << 26):
+    sel = (ftot >= lo) & (ftot < lo * 4 if lo else ftot < (1 << 12))
+    if sel.any():
+        t = cyc[sel].sum() / ghz / 1e3
+        print(f"    [{lo:>9}, x4): {sel.sum():5d} {t:7.3f} ms {1e3 * t / sel.sum():8.2f} us "
+              f"{ftot[sel].sum() / max(t, 1e-9) / 1e6:7.1f}")
 small = ftot < 4096
 print(f"  rounds with < 4096 arcs: {small.sum()} taking {cyc[small].sum()/ghz/1e3:.2f}ms "
       f"({cyc[small].mean()/ghz:.2f}us each); others {(~small).sum()} taking {cyc[~small].sum()/ghz/1e3:.2f}ms")
