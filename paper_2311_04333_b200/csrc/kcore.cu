@@ -41,8 +41,14 @@ constexpr int KC_THREADS = 1024;
 #define DG_KC_SPEC 1
 #endif
 constexpr uint32_t CH = 32;     // arcs per chunk = one warp step
-constexpr int UC = 2;           // chunks in flight per warp (short-row steps)
+#ifndef DG_UC
+#define DG_UC 2
+#endif
+constexpr int UC = DG_UC;         // chunks in flight per warp (short-row steps)
 constexpr int SC = 8;           // chunks per super-chunk (one warp step on long rows)
+#ifndef DG_WIDE_Q
+#define DG_WIDE_Q 2  // super-chunk rounds: at least DG_WIDE_Q / 4 super-chunks per warp
+#endif
 #ifndef DG_KC_HUBS
 #define DG_KC_HUBS 4096         // big rounds: decrements of ids below this summed per CTA
 #endif
@@ -820,7 +826,7 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
     // frontier's virtual arc space per warp step; rounds too small to give
     // every warp two super-chunks keep one 32-arc chunk per step (UC in
     // flight), so their work spreads over the whole grid
-    const bool wide = (Ftot + CH - 1) / CH >= uint64_t(nwarps) * SC * 2;
+    const bool wide = (Ftot + CH - 1) / CH * 4 >= uint64_t(nwarps) * SC * DG_WIDE_Q;
     {
       const Frontier& F = a.fr[f & 1];
       const uint32_t b32 = uint32_t(bound);
@@ -832,7 +838,10 @@ __global__ void __launch_bounds__(KC_THREADS, 1) k_coreness(KcArgs a) {
           load_chunks<UC>(F, a.adj, cb, nwarps, nch, Fc, Ftot, lane, u);
           expand_targets<BM, UC>(a, u, b32, s, nacc);
         }
-      for (uint64_t sc = gwarp; sc < nsc; sc += nwarps) {
+      // super-chunks go warp-major across the CTAs, so a round of fewer
+      // super-chunks than warps still spreads over every SM
+      const uint64_t swarp = uint64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+      for (uint64_t sc = swarp; sc < nsc; sc += nwarps) {
         const uint64_t c0 = sc * SC;
         const uint64_t clast = min(c0 + SC, nch) - 1;
         const uint64_t e0 = F.cse[c0];
