@@ -396,6 +396,15 @@ def run_ours(args, cfg, rank, world, local):
                    "witness_size": len(res[0].witness)},
         "gpu_launches": int(launches),
         "clocks": clk,
+        # where one step's device time goes (ms, mean over the timed steps)
+        "step_split": {
+            "kcore_kernel": kc_ms / args.steps,
+            "coreness_incl_get_core": sum(r.trace.init.coreness_ms for r in res) / args.steps,
+            "init_total": sum(r.trace.init.init_ms for r in res) / args.steps,
+            "iterations": it_ms / args.steps,
+            "reprune": sum(r.reprune_ms for r in res) / args.steps,
+            "host_total": sum(r.total_ms for r in res) / args.steps,
+            "device_total": dev_ms / args.steps},
     }
 
     # ---- the GreedySorting++ variant on the same graph,

@@ -435,7 +435,13 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
   const bool slice_smem = PT == 512 && g.maxdeg < 65536 &&
                           peelc::smem_bytes(nc, offs_smem, n) <= kSmemCap &&
                           !getenv("DG_NO_SLICE_SMEM");
-  const size_t smem = peelc::smem_bytes(nc, offs_smem, slice_smem ? n : 0);
+  // slice cache: 16 slots of up to 256 quads (4 KB) in what shared memory is left
+  uint32_t slotq = 0;
+  if (slice_smem && !getenv("DG_NO_SLICE_CACHE"))
+    for (uint32_t q = getenv("DG_SLICE_SLOTQ") ? atoi(getenv("DG_SLICE_SLOTQ")) : 256;
+         q >= 32 && !slotq; q >>= 1)
+      if (peelc::smem_bytes(nc, offs_smem, n, q) <= kSmemCap) slotq = q;
+  const size_t smem = peelc::smem_bytes(nc, offs_smem, slice_smem ? n : 0, slotq);
   auto kern = peelc::k_peel_cluster<CS, PT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess) {
@@ -473,7 +479,7 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
   DG_CHECK_LAUNCH();
   peelc::Args a{g.offs.get(), g.adj.get(), uint32_t(n), d_loads, base, one ? 1 : 0,
                 nc, nc / PT, no, offs_smem ? 1 : 0, d_perm, d_raw, seg.get(),
-                slice_smem ? 1 : 0, d_batches, peel_prof_buffer()};
+                slice_smem ? 1 : 0, slotq, d_batches, peel_prof_buffer()};
   DG_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   count_launch();
   return true;

@@ -60,6 +60,15 @@ constexpr uint32_t kSliceMin = DG_SLICE_MIN;
 #ifndef DG_PEEL_PROF
 #define DG_PEEL_PROF 0
 #endif
+#ifndef DG_SC_FILL
+#define DG_SC_FILL 1
+#endif
+#ifndef DG_SC_HIT
+#define DG_SC_HIT 1
+#endif
+#ifndef DG_SC_GEN
+#define DG_SC_GEN 1
+#endif
 #ifndef DG_ROW_PREFETCH
 #define DG_ROW_PREFETCH 1
 #endif
@@ -82,6 +91,8 @@ struct Args {
   const uint32_t* seg;
   int slice_smem;  // this CTA's slice bounds of EVERY row staged in shared memory
                    // (u16 start | u16 end << 16; rows shorter than 2^16)
+  uint32_t slotq;  // slice cache: 16-byte quads per slot (0: no cache; 512-thread CTAs
+                   // with slice_smem only)
   unsigned long long* batches;
   unsigned long long* prof;  // [8] rank-0 thread-0 cycles: S1, S2, S3, batches, simple
 };
@@ -111,6 +122,13 @@ struct Fixed {
   // nwj = #warps serving member j); batches of more than NW members are
   // removed as one flat quad range (remove_flat)
   uint32_t wmap[MAXW][MAXW];
+  // slice cache (see k_peel_cluster): one mbarrier and one tag word per slot,
+  // tag = cached vertex id | phase parity of its copy << 31 (kNoTag: empty)
+  unsigned long long mbS[16];
+  uint32_t ctag[16];
+#if DG_PEEL_PROF
+  uint32_t prevc[2][16];  // previous batch's CTA candidates (slice-cache hit estimate)
+#endif
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -135,6 +153,16 @@ __device__ __forceinline__ void mbar_init(uint32_t bar) {
 __device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
+}
+constexpr uint32_t kNoTag = 0x7fffffffu;  // no vertex id reaches 2^31 - 1 (n < 2^28)
+// this CTA's shared memory <- global, completing bytes on the CTA's mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -192,6 +220,55 @@ __device__ __forceinline__ void remove_local(const uint4* adj4, uint32_t keys_s,
         for (int e = 0; e < 4; ++e) c += (ok[e] && Range<uint32_t>::in_batch(old[e]) && us[e] < vj);
         if (c) atomicAdd(rawj, 0ULL - c);
       }
+    }
+  }
+}
+
+// the same from a slice-cache slot: the slot holds the aligned quads that
+// cover the slice [oj, oj + dj) of member vj's row, the slice starting at arc
+// (oj & 3) of the slot
+#ifndef DG_SC_INLINE
+#define DG_SC_INLINE __forceinline__
+#endif
+template <bool ONE>
+__device__ DG_SC_INLINE void remove_cached(uint32_t slot_s, uint32_t keys_s, uint32_t a0,
+                                              uint32_t dj, uint32_t vj, uint32_t rk, uint32_t nwj,
+                                              uint32_t lane, uint32_t gbase, uint32_t NC,
+                                              unsigned long long* rawj) {
+  const uint32_t a1 = a0 + dj, nq = (a1 + 3) >> 2;
+  for (uint32_t q = rk * 32 + lane; q < nq; q += nwj * 32) {
+    uint32_t us[4];
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(us[0]), "=r"(us[1]), "=r"(us[2]), "=r"(us[3])
+                 : "r"(slot_s + (q << 4)));
+    bool ok[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t p = (q << 2) + e;
+      ok[e] = p >= a0 && p < a1 && us[e] - gbase < NC;
+    }
+    if (ONE) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (ok[e])
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(keys_s + ((us[e] - gbase) << 2)),
+                       "r"(0xffffffffu)
+                       : "memory");
+    } else {
+      uint32_t old[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        old[e] = 0;
+        if (ok[e])
+          asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                       : "=r"(old[e])
+                       : "r"(keys_s + ((us[e] - gbase) << 2)), "r"(0xffffffffu)
+                       : "memory");
+      }
+      unsigned long long c = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) c += (ok[e] && Range<uint32_t>::in_batch(old[e]) && us[e] < vj);
+      if (c) atomicAdd(rawj, 0ULL - c);
     }
   }
 }
@@ -288,8 +365,16 @@ __device__ __forceinline__ void scan_regs(uint32_t* keys, uint32_t lo, uint32_t 
 template <int CS, int PT>
 __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   constexpr uint32_t NW = PT / 32;
-  constexpr int UQ = PT >= 1024 ? 2 : 4;  // quads in flight per thread (64 registers at 1024)
+  // quads in flight per thread: 64 registers at 1024 threads allow 2; 512-thread
+  // CTAs mostly remove slices of at most one or two quads per thread, and one
+  // quad leaves the registers the slice cache needs (17.9K core: 1.906 us/batch
+  // at 4, 1.878 at 2, 1.849 at 1)
+#ifndef DG_UQ512
+#define DG_UQ512 1
+#endif
+  constexpr int UQ = PT >= 1024 ? 2 : DG_UQ512;
   static_assert(CS <= 16, "summary slots");
+  static_assert(sizeof(Fixed) % 16 == 0, "cache slots follow Fixed, 16-byte aligned");
   using R = Range<uint32_t>;
   cg::cluster_group cl = cg::this_cluster();
   const uint32_t rank = cl.block_rank();
@@ -303,6 +388,17 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
   Fixed& s = *reinterpret_cast<Fixed*>(
       smem + head + (PT == 512 && a.slice_smem ? ((size_t(a.n) * 4 + 15) & ~size_t(15)) : 0));
   const uint4* adj4 = reinterpret_cast<const uint4*>(a.adj);
+  // Slice cache (512-thread CTAs with the slice bounds in shared memory).  A
+  // CTA's candidate that loses a batch is a likely member of the next ones
+  // (RMAT-26's 17.9K core: 3 of 4 members were their CTA's candidate one batch
+  // earlier), so after the decode the last warp copies this CTA's slice of
+  // every such candidate's row into slot q (q = the candidate's CTA) with
+  // cp.async.bulk, completing on the slot's mbarrier; a member whose id matches
+  // a slot's tag is removed from shared memory instead of paying the L2 / HBM
+  // round trip of its row on the batch's critical path.
+  constexpr bool CACHE = PT == 512;
+  const uint32_t slotq = CACHE && a.slice_smem ? a.slotq : 0u;
+  uint4* cdata = reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(&s) + sizeof(Fixed));
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
   const uint32_t n = a.n, c = a.chunk, lo = tid * c, hi = lo + c;
   const uint32_t gbase = rank * NO;  // first global id owned by this CTA
@@ -337,6 +433,11 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       mbar_init(smem_u32(&s.mbA[k]));
       mbar_init(smem_u32(&s.mbB[k]));
     }
+    if constexpr (CACHE)
+      for (int k = 0; k < 16; ++k) {
+        mbar_init(smem_u32(&s.mbS[k]));
+        s.ctag[k] = kNoTag | (1u << 31);  // parity 1: "the previous phase" of a fresh mbarrier
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cl.sync();  // every CTA's mbarriers exist before the first push
@@ -368,6 +469,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       a.prof[16 + ((b + 1 - arm) * 16 + rank) * 12 + k] = clock64();
   };
   long long c1 = 0, c2 = 0, c3 = 0, tm = DG_PEEL_PROF ? clock64() : 0;
+#if DG_PEEL_PROF
+  unsigned long long chit[2] = {0, 0}, cmem[2] = {0, 0};
+#endif
   while (removed < n) {
     stamp(nbat, 0);
     const uint32_t par = uint32_t(nbat & 1);
@@ -479,7 +583,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     // ---- S2: every warp decodes the CS summaries (lane q <- CTA q)
     uint32_t rmin = R::DEAD, rcnt = 0, rfirst = 0, rdeg = 0;
     uint64_t rr0 = 0;
+    uint32_t ctreg = kNoTag;  // lane q: tag word of cache slot q
     if (lane < CS) {
+      if (CACHE && slotq) ctreg = s.ctag[lane];
       const uint4* rs = reinterpret_cast<const uint4*>(&s.sum[par][lane]);
       const uint4 p0 = rs[0], p1 = rs[1];
       rmin = p0.x;
@@ -493,6 +599,37 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     const uint32_t ownmask = __ballot_sync(~0u, own);
     const uint32_t total = __reduce_add_sync(~0u, own ? rcnt : 0u);
     const uint32_t bs = a.one ? 1u : total;
+    if (DG_SC_FILL && CACHE && slotq && w == NW - 1 && lane < CS && R::alive(rmin) && !own &&
+        (ctreg & kNoTag) != rfirst) {
+      // slot `lane` <- this CTA's slice of CTA `lane`'s candidate (no member of
+      // this batch is owned by that CTA, so nobody reads the slot now)
+      uint32_t s0, s1;
+      slice_of(rfirst, s0, s1);
+      const uint64_t qa = (rr0 + s0) >> 2, qb = (rr0 + s1 + 3) >> 2;
+      const uint32_t bar = smem_u32(&s.mbS[lane]);
+      uint32_t ph = ctreg >> 31, tag = kNoTag;
+      if (s1 > s0 && qb - qa <= slotq) {
+        mbar_wait(bar, ph);  // the slot's previous copy has landed
+        ph ^= 1u;
+        const uint32_t bytes = uint32_t(qb - qa) * 16u;
+        mbar_expect(bar, bytes);
+        bulk_g2s(smem_u32(cdata + lane * slotq), adj4 + qa, bytes, bar);
+        tag = rfirst;
+      }
+      s.ctag[lane] = tag | (ph << 31);
+    }
+#if DG_PEEL_PROF
+    if (rank == 0 && w == 0) {  // would a cache of last batch's candidates' slices hit?
+      const bool hit = own && nbat && s.prevc[par][lane] == rfirst;
+      const uint32_t hm = __ballot_sync(~0u, hit);
+      if (lane < CS) s.prevc[par ^ 1][lane] = rfirst;
+      if (lane == 0) {
+        const bool simple = a.one || total == uint32_t(__popc(ownmask));
+        chit[simple] += __popc(hm);
+        cmem[simple] += simple ? bs : uint32_t(__popc(ownmask));
+      }
+    }
+#endif
     if (a.one || total == uint32_t(__popc(ownmask))) {
       // ---- simple batch: owner lane L (CTA L) holds member #(owners below L)
       if (P) ++nsimple;
@@ -520,18 +657,33 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         const uint32_t vj = __shfl_sync(~0u, rfirst, lj);
         uint32_t dj = __shfl_sync(~0u, rdeg, lj);
         uint64_t oj = __shfl_sync(~0u, rr0, lj);
-        if (dj >= kSliceMin) {  // long row: only this CTA's slice
+        uint32_t tg = kNoTag;  // the tag of the member's CTA's slot
+        if constexpr (CACHE) tg = __shfl_sync(~0u, ctreg, lj);
+        const bool hit = DG_SC_HIT && CACHE && slotq && (tg & kNoTag) == vj;
+        unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
+        if (!hit) {
+          if (dj >= kSliceMin) {  // long row: only this CTA's slice
+            uint32_t s0, s1;
+            slice_of(vj, s0, s1);
+            oj += s0;
+            dj = s1 - s0;
+          }
+          stamp(nbat, 8);
+          if (bs == 1)
+            remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
+          else
+            remove_local<false, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
+        } else {  // this CTA's slice of the row sits in cache slot lj
           uint32_t s0, s1;
           slice_of(vj, s0, s1);
-          oj += s0;
-          dj = s1 - s0;
+          const uint32_t a0 = (uint32_t(oj) + s0) & 3u;
+          mbar_wait(smem_u32(&s.mbS[lj]), tg >> 31);
+          const uint32_t slot_s = smem_u32(cdata + lj * slotq);
+          if (bs == 1)
+            remove_cached<true>(slot_s, keys_s, a0, s1 - s0, vj, rk, nwj, lane, gbase, NO, rawj);
+          else
+            remove_cached<false>(slot_s, keys_s, a0, s1 - s0, vj, rk, nwj, lane, gbase, NO, rawj);
         }
-        unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
-        stamp(nbat, 8);
-        if (bs == 1)
-          remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
-        else
-          remove_local<false, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
       } else if constexpr (NW < 32) {  // lane j <- member j (the owner lane of rank j)
         const uint32_t lj = (lane < bs ? __fns(ownmask, 0, int(lane) + 1) : 0u) & 31u;
         remove_flat<PT>(adj4, keys_s, bs, __shfl_sync(~0u, rfirst, lj), __shfl_sync(~0u, rdeg, lj),
@@ -601,10 +753,21 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           // only this CTA's slice of the member's row
           uint32_t s0, s1;
           slice_of(mj.v, s0, s1);
-          remove_local<false, UQ>(adj4, keys_s,
-                                  (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, s1 - s0,
-                                  mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NO,
-                                  reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
+          uint32_t hm = 0;
+          if constexpr (CACHE && DG_SC_GEN)
+            if (slotq) hm = __ballot_sync(~0u, (ctreg & kNoTag) == mj.v);
+          if (hm) {
+            const uint32_t sl = __ffs(hm) - 1;
+            mbar_wait(smem_u32(&s.mbS[sl]), __shfl_sync(~0u, ctreg, sl) >> 31);
+            remove_cached<false>(smem_u32(cdata + sl * slotq), keys_s, (mj.r0lo + s0) & 3u, s1 - s0,
+                                 mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NO,
+                                 reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
+          } else {
+            remove_local<false, UQ>(adj4, keys_s,
+                                    (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, s1 - s0,
+                                    mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NO,
+                                    reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
+          }
         } else if constexpr (NW < SB) {
           Member mj = {0u, 0u, 0u, 0u};
           uint32_t s0 = 0, s1 = 0;
@@ -667,6 +830,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     removed += bs;
     ++nbat;
   }
+  if (CACHE && slotq && w == NW - 1 && lane < CS)  // no copy in flight at exit
+    mbar_wait(smem_u32(&s.mbS[lane]), s.ctag[lane] >> 31);
   if (rank == 0 && tid == 0) *a.batches = nbat;
   if (P) {
     if (a.prof) {
@@ -681,13 +846,18 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       a.prof[7] = CS;
     }
   }
+#if DG_PEEL_PROF
+  if (rank == 0 && tid == 0 && a.prof) {
+    a.prof[9] = chit[1], a.prof[10] = cmem[1], a.prof[11] = chit[0], a.prof[12] = cmem[0];
+  }
+#endif
   cl.sync();  // no CTA exits while a push into it could be in flight
 }
 
-inline size_t smem_bytes(uint32_t nc, bool offs_smem, uint64_t slice_n = 0) {
+inline size_t smem_bytes(uint32_t nc, bool offs_smem, uint64_t slice_n = 0, uint32_t slotq = 0) {
   const size_t NC = nc;
   return ((NC * 4 * (offs_smem ? 2 : 1) + 4 + 15) & ~size_t(15)) +
-         ((slice_n * 4 + 15) & ~size_t(15)) + sizeof(Fixed);
+         ((slice_n * 4 + 15) & ~size_t(15)) + sizeof(Fixed) + size_t(slotq) * 16 * 16;
 }
 
 }  // namespace peelc

@@ -668,3 +668,37 @@ def test_peel_large_cores_cluster_and_global_keys(dg, orc):
         dg.density_and_load_update(g, p, ld)
         _, lh, _, _ = orc.density_update(core, p, lh)
         assert np.array_equal(ld, lh)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("slotq", ["256", "32", "off"])
+def test_peel_cluster_slice_cache(dg, orc, slotq):
+    """The cluster kernel's slice cache (peel_cluster.cuh: losing candidates'
+    row slices copied into shared-memory slots with cp.async.bulk, members
+    found there removed from shared memory) on a dense core, where a CTA's
+    slices run to ~60 quads: default slots, slots of 32 quads (most slices do
+    not fit and take the global path) and no cache give the reference
+    restatement's peel order and loads (refine.cpp:20-220), batch and
+    one-at-a-time."""
+    n = 18000
+    u, v = orc.gen_er_planted(n, 2200 * n, 500, 11)
+    h = orc.build(u, v)
+    g = dg.Graph.from_csr(h.offs, h.adj, h.orig)
+    rng = np.random.default_rng(7)
+    ld = rng.integers(0, 600, h.n).astype(np.uint64)
+    lh = ld.copy()
+    key = "DG_NO_SLICE_CACHE" if slotq == "off" else "DG_SLICE_SLOTQ"
+    os.environ[key] = "1" if slotq == "off" else slotq
+    dg.set_peel_mode(2)
+    try:
+        for it in range(2):
+            p = dg.load_peel_order(g, ld).perm
+            assert np.array_equal(p, orc.peel_order(h, lh, False)), (slotq, it)
+            dg.density_and_load_update(g, p, ld)
+            _, lh, _, _ = orc.density_update(h, p, lh)
+            assert np.array_equal(ld, lh), (slotq, it)
+        p = dg.load_peel_order(g, ld, one_at_a_time=True).perm
+        assert np.array_equal(p, orc.peel_order(h, lh, True)), slotq
+    finally:
+        dg.set_peel_mode(0)
+        del os.environ[key]
