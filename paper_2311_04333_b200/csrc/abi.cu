@@ -127,7 +127,8 @@ __global__ void k_witness(const uint64_t* orig, const uint32_t* perm, uint64_t f
 }
 
 __global__ void k_mark_witness(const uint64_t* orig, uint64_t n, const uint64_t* wit,
-                               uint64_t nwit, uint8_t* in, uint32_t* dense, uint32_t* err) {
+                               uint64_t nwit, uint32_t* in_bits, uint32_t* dense,
+                               uint32_t* err) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nwit;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t id = wit[i];
@@ -143,21 +144,9 @@ __global__ void k_mark_witness(const uint64_t* orig, uint64_t n, const uint64_t*
       *err = 1;
       continue;
     }
-    in[lo] = 1;
+    atomicOr(in_bits + (lo >> 5), 1u << (lo & 31));
     dense[i] = uint32_t(lo);
   }
-}
-
-__global__ void k_witness_arcs(const uint64_t* offs, const uint32_t* adj, const uint32_t* dense,
-                               uint64_t nwit, const uint8_t* in, unsigned long long* arcs) {
-  const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  unsigned long long c = 0;
-  for (uint64_t i = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; i < nwit; i += warps) {
-    const uint32_t v = dense[i];
-    for (uint64_t p = offs[v] + lane_id(); p < offs[v + 1]; p += 32) c += in[adj[p]];
-  }
-  c = warp_sum(c);
-  if (lane_id() == 0 && c) atomicAdd(arcs, c);
 }
 
 void sort_u64(uint64_t* d, uint64_t n) {
@@ -395,23 +384,20 @@ void run_impl(const dg_graph* g, const dg_run_config* cfg, dg_run_result* res,
   Nvtx rw("dg.witness");
   sort_u64(wit.get(), nwit);
   {
-    DevBuf<uint8_t> in(g->n);
+    DevBuf<uint32_t> in((g->n + 31) / 32);  // witness membership, one bit per input vertex
     in.zero();
     DevBuf<uint32_t> dense(std::max<uint64_t>(nwit, 1)), err(1);
-    DevBuf<unsigned long long> arcs(1);
     err.zero();
-    arcs.zero();
+    uint64_t arcs = 0;
     if (nwit) {
       k_mark_witness<<<grid_for(nwit, 256), 256, 0, stream()>>>(g->orig.get(), g->n, wit.get(),
                                                                 nwit, in.get(), dense.get(),
                                                                 err.get());
       DG_CHECK_LAUNCH();
       if (read_scalar(err.get())) throw DgError(DG_E_INVARIANT, "witness vertex not in input graph");
-      k_witness_arcs<<<grid_for(nwit * 32, 256), 256, 0, stream()>>>(
-          g->offs.get(), g->adj.get(), dense.get(), nwit, in.get(), arcs.get());
-      DG_CHECK_LAUNCH();
+      arcs = count_arcs_into_set(*g, dense.get(), nwit, in.get());
     }
-    res->witness_edges = read_scalar(arcs.get()) / 2;
+    res->witness_edges = arcs / 2;
     if (u128(res->witness_edges) * res->best_verts != u128(res->best_edges) * nwit)
       throw DgError(DG_E_INVARIANT, "witness does not reproduce the reported density");
   }

@@ -48,6 +48,10 @@ uint64_t device_max_degree(const uint64_t* d_offs, uint64_t n);
 // null).  d_old_to_new (device, n entries) is optional.
 GraphPtr induced(const dg_graph& g, const uint8_t* d_keep, const uint32_t* d_labels, uint32_t k,
                  uint32_t* d_old_to_new);
+// Arcs of the rows d_rows[0..nrows) whose target is in the vertex set d_bits
+// (a bitmap over g's n ids): the witness recount of framework.cpp:159-175.
+uint64_t count_arcs_into_set(const dg_graph& g, const uint32_t* d_rows, uint64_t nrows,
+                             const uint32_t* d_bits);
 // out[map[v]] = in[v] for kept v (labels / loads carried across a prune).
 void gather_by_map_u32(const uint32_t* in, const uint32_t* map, uint64_t n, uint32_t* out);
 void gather_by_map_u64(const uint64_t* in, const uint32_t* map, uint64_t n, uint64_t* out);
