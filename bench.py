@@ -553,6 +553,20 @@ def run_sharded(args, cfg, rank, world, local):
                     "core_n_m": [r0.trace.init.pruned_n, r0.trace.init.pruned_m],
                     "best": [r0.best.edges, r0.best.verts]},
         "greedy": {"iterations": len(iters), "ms_per_iter": it_ms_max / max(1, len(iters))},
+        # Greedy++ iteration roofline as at N=1 (8m + 28n + 8 bytes over t_iter)
+        "roofline": {"bound": "hbm",
+                     "achieved": sum(8 * it.m + 28 * it.n + 8 for it in iters) / (it_ms / 1e3) / 1e9,
+                     "peak": hbm, "unit": "GB/s",
+                     "frac": sum(8 * it.m + 28 * it.n + 8 for it in iters) / (it_ms / 1e3) / 1e9 / hbm,
+                     "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "Greedy++ iteration (replicated): k_peel_cluster / k_peel + k_alg3"},
+        # the sharded pipeline has no host input: every rank generates its slice of the
+        # seeded samples on its GPU, so this is the whole pipeline (generation, build,
+        # k-core, prune, gather, T iterations) timed on the device, not a host-buffer e2e
+        "e2e": {"value": edges / step_max, "unit": "edges/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(4 * n),
+                "includes": "per-rank generation + distributed build + sharded k-core + prune + "
+                            "gather + T iterations; labels read back to the host"},
         "gpu_launches": int(launches),
         "clocks": clk,
         "value_note": "Greedy++ runs replicated on the gathered core: value counts one replica's "

@@ -441,6 +441,13 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cl.sync();  // every CTA's mbarriers exist before the first push
+#ifndef DG_WMAP_REG
+#define DG_WMAP_REG 1
+#endif
+  // this warp's column of the warp -> member map, lane b - 1 <- wmap[b - 1][w]:
+  // a shuffle per batch instead of a dependent shared load (512-thread CTAs)
+  uint32_t wmreg = 0;
+  if (DG_WMAP_REG && PT == 512 && lane < NW) wmreg = s.wmap[lane][w];
 
   // CTA `rank`'s slice [s0, s1) of row v (offsets inside the row)
   // (512-thread CTAs only: the cores large enough for 1024-thread CTAs never
@@ -651,7 +658,8 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       }
       __syncwarp();
       if (bs <= NW) {
-        const uint32_t wm3 = s.wmap[bs - 1][w];
+        const uint32_t wm3 = DG_WMAP_REG && PT == 512 ? __shfl_sync(~0u, wmreg, bs - 1)
+                                                      : s.wmap[bs - 1][w];
         const uint32_t j = wm3 & 0xffu, rk = (wm3 >> 8) & 0xffu, nwj = wm3 >> 16;
         const uint32_t lj = __ffs(__ballot_sync(~0u, own && rkl == j)) - 1;
         const uint32_t vj = __shfl_sync(~0u, rfirst, lj);
@@ -661,6 +669,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         if constexpr (CACHE) tg = __shfl_sync(~0u, ctreg, lj);
         const bool hit = DG_SC_HIT && CACHE && slotq && (tg & kNoTag) == vj;
         unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
+        stamp(nbat, 8);
         if (!hit) {
           if (dj >= kSliceMin) {  // long row: only this CTA's slice
             uint32_t s0, s1;
@@ -668,7 +677,6 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
             oj += s0;
             dj = s1 - s0;
           }
-          stamp(nbat, 8);
           if (bs == 1)
             remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
           else
