@@ -501,6 +501,11 @@ bool launch_cluster(const dg_graph& g, const uint64_t* d_loads, uint64_t base, b
   int pt = per_cta <= 4096 ? 512 : 1024;
   if (const char* e = getenv("DG_CLUSTER_PT")) pt = atoi(e) == 512 ? 512 : 1024;
   uint64_t c = (per_cta + pt - 1) / pt;  // keys per thread
+  // an odd number of keys per thread: S1's scalar shared loads at an even
+  // word stride hit each bank from 2 (4 at stride 4) lanes of the warp
+  // (ncu on the 84K core at 6 keys: 52 % of its shared wavefronts were
+  // excess); 8 stays (the two-vector tier)
+  if (c < 8 && (c & 1) == 0 && !getenv("DG_CLUSTER_EVEN")) ++c;
   if (getenv("DG_CLUSTER_POW2") && getenv("DG_CLUSTER_POW2")[0] == '1') {
     uint64_t nc = 512;
     while (nc * CS < g.n) nc *= 2;

@@ -111,7 +111,11 @@ struct __align__(16) Member {
 
 struct Fixed {
   unsigned long long mbA[2], mbB[2];  // summaries / staged members, by parity
-  Summary sum[2][16];                 // [parity][CTA rank]
+  // the summaries' halves in separate arrays, [parity][CTA rank]: lane q's
+  // 16-byte loads sit at a 16-byte stride (conflict free; the 32-byte stride
+  // of whole Summary slots doubled their wavefronts)
+  uint4 sumA[2][16];                  // min key, count, first id, degree
+  uint4 sumB[2][16];                  // row start (u64), pad
   Member stage[2][SB];                // [parity][member]
   // per-warp summary: {min key, #keys at it, first index at it, its row start}
   // and that row's degree (row bounds only with offsets staged in shared memory)
@@ -573,10 +577,11 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
 #endif
       stamp(nbat, 7);
       if (lane < CS) {
-        const uint32_t dst = mapa(smem_u32(&s.sum[par][rank]), lane);
         const uint32_t bar = mapa(mbA, lane);
-        st_async(dst, make_uint4(cm, ccnt, gbase + f, uint32_t(r1 - r0)), bar);
-        st_async(dst + 16, make_uint4(uint32_t(r0), uint32_t(r0 >> 32), 0u, 0u), bar);
+        st_async(mapa(smem_u32(&s.sumA[par][rank]), lane),
+                 make_uint4(cm, ccnt, gbase + f, uint32_t(r1 - r0)), bar);
+        st_async(mapa(smem_u32(&s.sumB[par][rank]), lane),
+                 make_uint4(uint32_t(r0), uint32_t(r0 >> 32), 0u, 0u), bar);
       }
     }
     stamp(nbat, 1);
@@ -593,8 +598,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     uint32_t ctreg = kNoTag;  // lane q: tag word of cache slot q
     if (lane < CS) {
       if (CACHE && slotq) ctreg = s.ctag[lane];
-      const uint4* rs = reinterpret_cast<const uint4*>(&s.sum[par][lane]);
-      const uint4 p0 = rs[0], p1 = rs[1];
+      const uint4 p0 = s.sumA[par][lane], p1 = s.sumB[par][lane];
       rmin = p0.x;
       rcnt = p0.y;
       rfirst = p0.z;

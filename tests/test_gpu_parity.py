@@ -530,9 +530,10 @@ print("ok")
 @pytest.mark.parametrize("n", [30000, 45000, 60000, 75000, 120000])
 def test_peel_cluster_chunk_tiers(dg, orc, n):
     """The cluster Greedy++ kernel (mode 2) across its S1 register tiers and
-    CTA sizes: per-CTA blocks of ceil(n/16) ids give 4, 6 and 8 keys per
-    thread at 512 threads (8: the two-vector load) and 5 and 8 at 1024
-    threads; the peel order (batch and one-at-a-time) and loads over three
+    CTA sizes: per-CTA blocks of ceil(n/16) ids need 4, 6 and 8 keys per
+    thread at 512 threads and 5 and 8 at 1024 threads; even counts below 8
+    are rounded up to odd ones (conflict-free scans), 8 is the two-vector
+    load; the peel order (batch and one-at-a-time) and loads over three
     Greedy++ iterations equal the reference restatement's (refine.cpp:20-220)."""
     u, v = orc.gen_er_planted(n, 10 * n, 60, n % 97)
     h = orc.build(u, v)
