@@ -54,6 +54,12 @@ constexpr int SB = 32;  // staged (small) batch members
 #endif
 // simple batches read only the CTA's slice of rows at least this long
 constexpr uint32_t kSliceMin = DG_SLICE_MIN;
+// 1024-thread CTAs look their slice up in the global table (a dependent
+// round trip before the row's) and cover 4K arcs per pass
+#ifndef DG_SLICE_MIN_1024
+#define DG_SLICE_MIN_1024 2048
+#endif
+constexpr uint32_t kSliceMin1024 = DG_SLICE_MIN_1024;
 // DG_PEEL_PROF=1 (a tuning build: python build.py prof -DDG_PEEL_PROF=1)
 // records rank-0 phase cycles into Args::prof; the production kernel carries
 // none of those live registers.
@@ -376,7 +382,13 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
 #ifndef DG_UQ512
 #define DG_UQ512 1
 #endif
-  constexpr int UQ = PT >= 1024 ? 2 : DG_UQ512;
+  // (1024 threads: one quad too -- RMAT-26's 84K core 3.42 -> 3.12 us/batch,
+  // RMAT-28's 122K core 3.52 -> 3.19, 56 registers instead of 64: a pass of the
+  // CTA covers 4K arcs, so the second quad was almost always predicated off)
+#ifndef DG_UQ1024
+#define DG_UQ1024 1
+#endif
+  constexpr int UQ = PT >= 1024 ? DG_UQ1024 : DG_UQ512;
   static_assert(CS <= 16, "summary slots");
   static_assert(sizeof(Fixed) % 16 == 0, "cache slots follow Fixed, 16-byte aligned");
   using R = Range<uint32_t>;
@@ -675,7 +687,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
         stamp(nbat, 8);
         if (!hit) {
-          if (dj >= kSliceMin) {  // long row: only this CTA's slice
+          if (dj >= (PT >= 1024 ? kSliceMin1024 : kSliceMin)) {  // long row: only this CTA's slice
             uint32_t s0, s1;
             slice_of(vj, s0, s1);
             oj += s0;
