@@ -429,6 +429,8 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
                        unsigned long long* d_batches) {
   const uint64_t n = g.n;
   const bool offs32 = 2 * g.m < 0xffffffffULL;
+  // 64-bit row offsets in the kernel (DG_CLUSTER_O64=1 forces them: tests)
+  const bool o64 = 2 * g.m + 64 >= 0xffffffffULL || getenv("DG_CLUSTER_O64");
   bool offs_smem = offs32 && peelc::smem_bytes(nc, true) <= kSmemCap;
   if (!offs_smem && peelc::smem_bytes(nc, false) > kSmemCap) return false;
   // every row's slice bounds in shared memory when they fit (rows < 2^16 arcs)
@@ -442,7 +444,7 @@ bool launch_cluster_pt(const dg_graph& g, const uint64_t* d_loads, uint64_t base
          q >= 32 && !slotq; q >>= 1)
       if (peelc::smem_bytes(nc, offs_smem, n, q) <= kSmemCap) slotq = q;
   const size_t smem = peelc::smem_bytes(nc, offs_smem, slice_smem ? n : 0, slotq);
-  auto kern = peelc::k_peel_cluster<CS, PT>;
+  auto kern = o64 ? peelc::k_peel_cluster<CS, PT, true> : peelc::k_peel_cluster<CS, PT, false>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
       cudaSuccess) {
     cudaGetLastError();

@@ -185,26 +185,26 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 
 // row [oj, oj + dj) of member vj, quads [rk*32 + lane, ...) step nwj*32:
 // decrement the targets in this CTA's block [gbase, gbase + NC)
-template <bool ONE, int UQ>
-__device__ __forceinline__ void remove_local(const uint4* adj4, uint32_t keys_s, uint64_t oj,
+template <bool ONE, int UQ, class Off = uint64_t>
+__device__ __forceinline__ void remove_local(const uint4* adj4, uint32_t keys_s, Off oj,
                                              uint32_t dj, uint32_t vj, uint32_t rk, uint32_t nwj,
                                              uint32_t lane, uint32_t gbase, uint32_t NC,
                                              unsigned long long* rawj) {
-  const uint64_t ej = oj + dj, q1 = (ej + 3) >> 2, stride = uint64_t(nwj) * 32;
-  for (uint64_t b0 = (oj >> 2) + uint64_t(rk) * 32 + lane; b0 < q1; b0 += stride * UQ) {
+  const Off ej = oj + dj, q1 = (ej + 3) >> 2, stride = Off(nwj) * 32;
+  for (Off b0 = (oj >> 2) + Off(rk) * 32 + lane; b0 < q1; b0 += stride * UQ) {
     uint4 x[UQ];
 #pragma unroll
     for (int k = 0; k < UQ; ++k)
       if (b0 + k * stride < q1) x[k] = __ldg(adj4 + b0 + k * stride);
 #pragma unroll
     for (int k = 0; k < UQ; ++k) {
-      const uint64_t q = b0 + k * stride;
+      const Off q = b0 + k * stride;
       if (q >= q1) break;
       const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
       bool ok[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const uint64_t p = (q << 2) + e;
+        const Off p = (q << 2) + e;
         ok[e] = p >= oj && p < ej && us[e] - gbase < NC;
       }
       if (ONE) {
@@ -288,9 +288,9 @@ __device__ DG_SC_INLINE void remove_cached(uint32_t slot_s, uint32_t keys_s, uin
 // j: id, degree, row start), 2 quads per thread per round over the CTA, each
 // quad's member found by a 5-step binary search over the lanes' prefix
 // sums.  Every thread gets the same share however the batch's degrees vary.
-template <int PT>
+template <int PT, class Off = uint64_t>
 __device__ __forceinline__ void remove_flat(const uint4* adj4, uint32_t keys_s, uint32_t bs,
-                                            uint32_t mv, uint32_t mdeg, uint64_t mr0,
+                                            uint32_t mv, uint32_t mdeg, Off mr0,
                                             uint32_t w, uint32_t lane, uint32_t gbase,
                                             uint32_t NC, unsigned long long* rawpos) {
   const uint32_t nq = lane < bs ? (uint32_t(mr0 & 3) + mdeg + 3) >> 2 : 0u;
@@ -310,24 +310,24 @@ __device__ __forceinline__ void remove_flat(const uint4* adj4, uint32_t keys_s, 
         if (e <= t) lo = mid; else hi = mid - 1;
       }
       m[k] = lo;
-      const uint64_t r0 = __shfl_sync(~0u, mr0, lo);
+      const Off r0 = __shfl_sync(~0u, mr0, lo);
       const uint32_t ex = __shfl_sync(~0u, excl, lo);
       if (t < totq) x[k] = __ldg(adj4 + (r0 >> 2) + (t - ex));
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const uint32_t t = base + k * PT + lane;
-      const uint64_t r0 = __shfl_sync(~0u, mr0, m[k]);
+      const Off r0 = __shfl_sync(~0u, mr0, m[k]);
       const uint32_t d = __shfl_sync(~0u, mdeg, m[k]), v = __shfl_sync(~0u, mv, m[k]);
       const uint32_t ex = __shfl_sync(~0u, excl, m[k]);
       if (t >= totq) continue;
-      const uint64_t q = (r0 >> 2) + (t - ex);
+      const Off q = (r0 >> 2) + (t - ex);
       const uint32_t us[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
       uint32_t old[4];
       bool ok[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const uint64_t pp = (q << 2) + e;
+        const Off pp = (q << 2) + e;
         ok[e] = pp >= r0 && pp < r0 + d && us[e] - gbase < NC;
         old[e] = 0;
         if (ok[e])
@@ -372,8 +372,11 @@ __device__ __forceinline__ void scan_regs(uint32_t* keys, uint32_t lo, uint32_t 
   for (int j = 0; j < KR; ++j) bits |= uint32_t(k[j] == lmin) << j;
 }
 
-template <int CS, int PT>
+// O64: row offsets beyond 32 bits (2m + 16 >= 2^32); the usual core's fit a
+// u32, which halves the offset arithmetic and shuffles on the batch's chain
+template <int CS, int PT, bool O64>
 __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
+  using Off = std::conditional_t<O64, uint64_t, uint32_t>;
   constexpr uint32_t NW = PT / 32;
   // quads in flight per thread: 64 registers at 1024 threads allow 2; 512-thread
   // CTAs mostly remove slices of at most one or two quads per thread, and one
@@ -606,7 +609,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
     }
     // ---- S2: every warp decodes the CS summaries (lane q <- CTA q)
     uint32_t rmin = R::DEAD, rcnt = 0, rfirst = 0, rdeg = 0;
-    uint64_t rr0 = 0;
+    Off rr0 = 0;
     uint32_t ctreg = kNoTag;  // lane q: tag word of cache slot q
     if (lane < CS) {
       if (CACHE && slotq) ctreg = s.ctag[lane];
@@ -615,7 +618,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       rcnt = p0.y;
       rfirst = p0.z;
       rdeg = p0.w;
-      rr0 = uint64_t(p1.x) | (uint64_t(p1.y) << 32);
+      rr0 = O64 ? Off(uint64_t(p1.x) | (uint64_t(p1.y) << 32)) : Off(p1.x);
     }
     const uint32_t gmin = __reduce_min_sync(~0u, rmin);
     const bool own = lane < CS && rmin == gmin;
@@ -628,7 +631,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       // this batch is owned by that CTA, so nobody reads the slot now)
       uint32_t s0, s1;
       slice_of(rfirst, s0, s1);
-      const uint64_t qa = (rr0 + s0) >> 2, qb = (rr0 + s1 + 3) >> 2;
+      const Off qa = (rr0 + s0) >> 2, qb = (rr0 + s1 + 3) >> 2;
       const uint32_t bar = smem_u32(&s.mbS[lane]);
       uint32_t ph = ctreg >> 31, tag = kNoTag;
       if (s1 > s0 && qb - qa <= slotq) {
@@ -680,7 +683,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         const uint32_t lj = __ffs(__ballot_sync(~0u, own && rkl == j)) - 1;
         const uint32_t vj = __shfl_sync(~0u, rfirst, lj);
         uint32_t dj = __shfl_sync(~0u, rdeg, lj);
-        uint64_t oj = __shfl_sync(~0u, rr0, lj);
+        Off oj = __shfl_sync(~0u, rr0, lj);
         uint32_t tg = kNoTag;  // the tag of the member's CTA's slot
         if constexpr (CACHE) tg = __shfl_sync(~0u, ctreg, lj);
         const bool hit = DG_SC_HIT && CACHE && slotq && (tg & kNoTag) == vj;
@@ -694,9 +697,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
             dj = s1 - s0;
           }
           if (bs == 1)
-            remove_local<true, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
+            remove_local<true, UQ, Off>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
           else
-            remove_local<false, UQ>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
+            remove_local<false, UQ, Off>(adj4, keys_s, oj, dj, vj, rk, nwj, lane, gbase, NO, rawj);
         } else {  // this CTA's slice of the row sits in cache slot lj
           uint32_t s0, s1;
           slice_of(vj, s0, s1);
@@ -710,7 +713,7 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         }
       } else if constexpr (NW < 32) {  // lane j <- member j (the owner lane of rank j)
         const uint32_t lj = (lane < bs ? __fns(ownmask, 0, int(lane) + 1) : 0u) & 31u;
-        remove_flat<PT>(adj4, keys_s, bs, __shfl_sync(~0u, rfirst, lj), __shfl_sync(~0u, rdeg, lj),
+        remove_flat<PT, Off>(adj4, keys_s, bs, __shfl_sync(~0u, rfirst, lj), __shfl_sync(~0u, rdeg, lj),
                     __shfl_sync(~0u, rr0, lj), w, lane, gbase, NO,
                     reinterpret_cast<unsigned long long*>(&a.raw[pos]));
       }
@@ -787,10 +790,11 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
                                  mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NO,
                                  reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
           } else {
-            remove_local<false, UQ>(adj4, keys_s,
-                                    (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, s1 - s0,
-                                    mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NO,
-                                    reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
+            remove_local<false, UQ, Off>(
+                adj4, keys_s,
+                (O64 ? Off(uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) : Off(mj.r0lo)) + s0,
+                s1 - s0, mj.v, (wm3 >> 8) & 0xffu, wm3 >> 16, lane, gbase, NO,
+                reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
           }
         } else if constexpr (NW < SB) {
           Member mj = {0u, 0u, 0u, 0u};
@@ -799,9 +803,10 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
             mj = s.stage[par][lane];
             slice_of(mj.v, s0, s1);
           }
-          remove_flat<PT>(adj4, keys_s, bs, mj.v, s1 - s0,
-                          (uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) + s0, w, lane, gbase, NO,
-                          reinterpret_cast<unsigned long long*>(&a.raw[pos]));
+          remove_flat<PT, Off>(
+              adj4, keys_s, bs, mj.v, s1 - s0,
+              (O64 ? Off(uint64_t(mj.r0lo) | (uint64_t(mj.r0hi) << 32)) : Off(mj.r0lo)) + s0, w, lane,
+              gbase, NO, reinterpret_cast<unsigned long long*>(&a.raw[pos]));
         }
         __syncthreads();
       } else {
@@ -818,13 +823,13 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           for (uint32_t g0 = 0; g0 < bs; g0 += 32) {
             const uint32_t gb = min(32u, bs - g0);
             uint32_t mv = 0, s0 = 0, s1 = 0;
-            uint64_t o = 0;
+            Off o = 0;
             if (lane < gb) {
               mv = a.perm[pos + g0 + lane];
-              o = a.offs[mv];
+              o = Off(a.offs[mv]);
               slice_of(mv, s0, s1);
             }
-            remove_flat<PT>(adj4, keys_s, gb, mv, s1 - s0, o + s0, w, lane, gbase, NO,
+            remove_flat<PT, Off>(adj4, keys_s, gb, mv, s1 - s0, o + s0, w, lane, gbase, NO,
                             reinterpret_cast<unsigned long long*>(&a.raw[pos + g0]));
           }
         } else {
@@ -833,10 +838,10 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
           // measured no faster there (84K core 3.83 vs 3.78 us/batch)
           for (uint32_t j = w; j < bs; j += NW) {
             const uint32_t vj = a.perm[pos + j];
-            const uint64_t oj = a.offs[vj];
+            const Off oj = Off(a.offs[vj]);
             uint32_t s0, s1;
             slice_of(vj, s0, s1);
-            remove_local<false, UQ>(adj4, keys_s, oj + s0, s1 - s0, vj, 0, 1, lane, gbase, NO,
+            remove_local<false, UQ, Off>(adj4, keys_s, oj + s0, s1 - s0, vj, 0, 1, lane, gbase, NO,
                                     reinterpret_cast<unsigned long long*>(&a.raw[pos + j]));
           }
         }

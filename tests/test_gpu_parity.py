@@ -703,3 +703,25 @@ def test_peel_cluster_slice_cache(dg, orc, slotq):
     finally:
         dg.set_peel_mode(0)
         del os.environ[key]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [30000, 75000])
+def test_peel_cluster_64bit_offsets(dg, orc, n):
+    """The cluster kernel's 64-bit row-offset instantiation (cores with 2m
+    beyond 32 bits; forced here by DG_CLUSTER_O64) at 512 and 1024 threads
+    gives the reference restatement's peel order, batch and one-at-a-time
+    (refine.cpp:20-156)."""
+    u, v = orc.gen_er_planted(n, 12 * n, 80, n % 89)
+    h = orc.build(u, v)
+    g = dg.Graph.from_csr(h.offs, h.adj, h.orig)
+    ld = np.random.default_rng(n + 1).integers(0, 40, h.n).astype(np.uint64)
+    os.environ["DG_CLUSTER_O64"] = "1"
+    dg.set_peel_mode(2)
+    try:
+        for one in (False, True):
+            p = dg.load_peel_order(g, ld, one_at_a_time=one).perm
+            assert np.array_equal(p, orc.peel_order(h, ld, one)), (n, one)
+    finally:
+        dg.set_peel_mode(0)
+        del os.environ["DG_CLUSTER_O64"]
