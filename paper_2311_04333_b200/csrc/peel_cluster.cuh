@@ -581,7 +581,10 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
       // pull its row into L2 while the summaries travel (cores whose
       // adjacency exceeds L2 -- RMAT-26's -- would otherwise pay an HBM
       // round trip on the removal's critical path)
-      if (lane == 0 && R::alive(cm) && r1 > r0) {
+      // (1024-thread CTAs only: at 512 the slice cache's fills bring the losers'
+      // rows in, and the prefetch sits on the push path -- 17.9K core 1.833 ->
+      // 1.802 without it)
+      if (PT >= 1024 && lane == 0 && R::alive(cm) && r1 > r0) {
         const uint64_t b0 = (r0 * 4) & ~uint64_t(15);
         const uint64_t b1 = min((r1 * 4 + 15) & ~uint64_t(15), b0 + (uint64_t(1) << 16));
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
@@ -690,7 +693,9 @@ __global__ void __launch_bounds__(PT, 1) k_peel_cluster(Args a) {
         unsigned long long* rawj = reinterpret_cast<unsigned long long*>(&a.raw[pos + j]);
         stamp(nbat, 8);
         if (!hit) {
-          if (dj >= (PT >= 1024 ? kSliceMin1024 : kSliceMin)) {  // long row: only this CTA's slice
+          // long row: only this CTA's slice; every row when the slice bounds are a
+          // shared load away (RMAT-22's 9.1K core in cluster mode 1.814 -> 1.767)
+          if (dj >= (PT >= 1024 ? kSliceMin1024 : kSliceMin) || (PT == 512 && a.slice_smem)) {
             uint32_t s0, s1;
             slice_of(vj, s0, s1);
             oj += s0;
