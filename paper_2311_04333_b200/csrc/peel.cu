@@ -37,6 +37,10 @@ constexpr uint64_t kQueueMinN = 16384;
 // vs cluster: 9.1K vertices (RMAT-22) 1.62 / 1.66, 10.9K (RMAT-23) 2.28 / 1.71,
 // 12.9K (RMAT-24) 2.31 / 1.77, 15.3K (RMAT-25) 2.63 / 1.79
 constexpr uint64_t kClusterMinN = 9600;
+// ... and smaller cores with long rows, whose removal one SM streams alone:
+// Chung-Lu 50M's 6.6K core (average degree 2,301) 1.85 / 1.74, while RMAT-22's
+// 9.1K core (1,373) stays on the single CTA
+constexpr uint64_t kClusterDenseMinN = 4096, kClusterDenseDeg = 2000;
 std::atomic<int> g_peel_mode{0};  // dg_set_peel_mode: 0 auto, 1 scanning single-CTA kernel, 2 cluster, 3 candidate list
 
 namespace {
@@ -556,7 +560,8 @@ void peel_order(const dg_graph& g, const uint64_t* d_loads, const KeyRange& kr,
   // 3.52 vs 4.22 us per batch for the candidate-list kernel, RMAT-26's 17.9K
   // core 2.98 vs 3.20), the candidate-list kernel when no cluster fits
   const int mode = g_peel_mode.load(std::memory_order_relaxed);
-  if (k32 && !one_at_a_time && mode == 0 && g.n > kClusterMinN) {
+  const bool dense_mid = g.n > kClusterDenseMinN && 2 * g.m >= kClusterDenseDeg * g.n;
+  if (k32 && !one_at_a_time && mode == 0 && (g.n > kClusterMinN || dense_mid)) {
     // DG_CLUSTER_CS=8 prefers the 8-CTA cluster (tuning)
     static const bool pref8 = getenv("DG_CLUSTER_CS") && atoi(getenv("DG_CLUSTER_CS")) == 8;
     if (pref8 && launch_cluster<8>(g, d_loads, base, false, d_perm, d_raw, d_batches)) return;
